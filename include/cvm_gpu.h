@@ -1,0 +1,249 @@
+/*
+ * cvm_gpu.h -- C ABI of the B200-native batched TFHE gate-bootstrapping
+ * backend (libcvm_b200.so).  Plain pointers and sizes only; no torch/CUDA types.
+ *
+ * Drop-in boundary.  The reference's gate seam is the abstract C++ class
+ * cryptovm::Backend (/root/reference/proj/core/include/cryptovm/gates.hpp:109-132):
+ * every functional unit (alu.cpp), Word helper (word.cpp) and the emulator
+ * (emulator.cpp) reach gates only through it.  A GPU backend replacing
+ * SimBackend (sim_backend.hpp:33-71) binds the entry points below; the shim a
+ * maintainer adds to the reference tree is shown in INTEGRATION.md.  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Conventions.  Every function returns CVM_OK (0) or a negative cvm_status;
+ * the message of the last failure on the calling thread is cvm_last_error().
+ * CVM_E_INPUT mirrors the reference's cryptovm::InputError (bad handle, bad
+ * gate kind, bad blob: sim_backend.cpp:47-49,53-57,80-83,124-126); CVM_E_DEVICE
+ * mirrors cryptovm::Error for device failures (errors.hpp:24-58).  There is no
+ * CPU fallback: without a usable sm_100a device, cvm_ctx_create fails.
+ */
+#ifndef CVM_GPU_H_
+#define CVM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVM_API __attribute__((visibility("default")))
+
+typedef enum cvm_status {
+  CVM_OK = 0,
+  CVM_E_INPUT = -1,       /* precondition violated (cryptovm::InputError)  */
+  CVM_E_DEVICE = -2,      /* CUDA failure / no sm_100a device              */
+  CVM_E_STATE = -3,       /* call out of order (e.g. gates before keys)    */
+  CVM_E_NOMEM = -4
+} cvm_status;
+
+/* Parameter set (TFHE default gate bootstrapping; BASELINE.json configs[0]). */
+#define CVM_LWE_N 630
+#define CVM_POLY_N 1024
+#define CVM_LWE_WORDS 631                    /* a[0..629], b : 2,524 B       */
+#define CVM_BK_WORDS (630u * 6u * 2u * 1024u) /* bk[i][row][poly][coef] u32   */
+#define CVM_KSK_WORDS (1024u * 8u * 4u * 631u) /* ksk[i][j][v][631] u32       */
+
+/* Gate kinds = cryptovm::GateKind enumerators (gates.hpp:31-46). */
+typedef enum cvm_gate_kind {
+  CVM_CONSTANT = 0, CVM_NOT = 1, CVM_COPY = 2, CVM_NAND = 3, CVM_AND = 4,
+  CVM_OR = 5, CVM_XOR = 6, CVM_XNOR = 7, CVM_NOR = 8, CVM_ANDNY = 9,
+  CVM_ANDYN = 10, CVM_ORNY = 11, CVM_ORYN = 12, CVM_MUX = 13
+} cvm_gate_kind;
+
+CVM_API const char* cvm_last_error(void);
+CVM_API const char* cvm_version(void);
+
+/* ------------------------------------------------------------------------
+ * Key owner (host).  Keygen / encrypt / decrypt stay on the host, as in the
+ * reference: Backend::encrypt_bit / decrypt_bit (gates.hpp:120-121),
+ * SimBackend::encrypt_bit / decrypt_bit (sim_backend.cpp:108-116),
+ * Word::encrypt / decrypt_word (word.cpp:42-86).
+ * ---------------------------------------------------------------------- */
+typedef struct cvm_keyset cvm_keyset;
+CVM_API int cvm_keyset_generate(uint64_t seed, cvm_keyset** out);
+CVM_API void cvm_keyset_destroy(cvm_keyset* ks);
+/* Export key material (lwe_key 630 i32, tlwe_key 1024 i32, bk, ksk u32). */
+CVM_API int cvm_keyset_export(const cvm_keyset* ks, int32_t* lwe_key,
+                              int32_t* tlwe_key, uint32_t* bk, uint32_t* ksk);
+/* Fresh encryptions of `count` bits (one seeded noise stream per call). */
+CVM_API int cvm_encrypt_bits(const cvm_keyset* ks, uint64_t seed, size_t count,
+                             const uint8_t* bits, uint32_t* out_lwe);
+CVM_API int cvm_decrypt_bits(const cvm_keyset* ks, size_t count,
+                             const uint32_t* lwe, uint8_t* bits, int32_t* phases);
+
+/* ------------------------------------------------------------------------
+ * Device context: one CUDA stream, bootstrapping key resident in HBM in FFT
+ * domain (59 MiB), key-switching key resident (79 MiB), a slab of LWE slots.
+ * ---------------------------------------------------------------------- */
+typedef struct cvm_ctx cvm_ctx;
+CVM_API int cvm_ctx_create(int device, cvm_ctx** out);
+CVM_API void cvm_ctx_destroy(cvm_ctx* ctx);
+/* Upload BK (time domain, CVM_BK_WORDS) and KSK (CVM_KSK_WORDS) once; the BK
+ * is transformed to the FFT domain on the device. */
+CVM_API int cvm_upload_keys(cvm_ctx* ctx, const uint32_t* bk, const uint32_t* ksk);
+CVM_API int cvm_upload_keyset(cvm_ctx* ctx, const cvm_keyset* ks);
+/* Hand out `n` fresh slot ids (bump allocator shared by every backend on the
+ * context); capacity follows at the next reserve or flush. */
+CVM_API int cvm_slots_alloc(cvm_ctx* ctx, uint64_t n, uint64_t* first);
+/* Ensure capacity for `n` LWE slots (slot ids 0..n-1). */
+CVM_API int cvm_slots_reserve(cvm_ctx* ctx, uint64_t n);
+CVM_API uint64_t cvm_slots_capacity(const cvm_ctx* ctx);
+/* Host <-> device ciphertext transfer, 631 u32 per slot, stream-ordered. */
+CVM_API int cvm_upload_lwe(cvm_ctx* ctx, uint64_t slot, uint64_t count,
+                           const uint32_t* lwe);
+CVM_API int cvm_download_lwe(cvm_ctx* ctx, uint64_t slot, uint64_t count,
+                             uint32_t* lwe);
+
+/* A gate operand is a linear form  sign * slot + constant  (torus32): NOT,
+ * COPY and CONSTANT (gates.hpp:113-114, sim_backend.cpp:75-88) fold into it,
+ * so only bootstrapped gates reach the device. slot < 0: pure constant. */
+typedef struct cvm_operand {
+  int64_t slot;
+  int32_t sign;       /* +1 or -1 */
+  uint32_t constant;  /* added to the b word */
+} cvm_operand;
+
+/* One bootstrapped gate: Backend::binary_gate (gates.hpp:115) for kinds
+ * NAND..ORYN with in[0], in[1]; Backend::mux_gate (gates.hpp:116-118) for MUX
+ * with in[0]=sel, in[1]=on_true, in[2]=on_false. */
+typedef struct cvm_gate {
+  uint32_t kind;
+  uint32_t pad;
+  cvm_operand in[3];
+  uint64_t out_slot;
+} cvm_gate;
+
+/* Enqueue one dataflow level: `count` mutually independent gates whose inputs
+ * are slots written by earlier levels or uploads.  Asynchronous. */
+CVM_API int cvm_submit_level(cvm_ctx* ctx, const cvm_gate* gates, uint64_t count);
+/* Wait for everything enqueued on the context. */
+CVM_API int cvm_sync(cvm_ctx* ctx);
+
+/* Kernel accounting: when enabled, each launch is bracketed by CUDA events on
+ * the context stream; totals are resolved at cvm_sync. */
+typedef struct cvm_kernel_stats {
+  uint64_t br_launches, br_jobs;   /* blind rotations (bootstraps)       */
+  uint64_t ks_launches, ks_jobs;   /* key switches                       */
+  uint64_t other_launches;
+  double br_ms, ks_ms;             /* summed event time                  */
+} cvm_kernel_stats;
+CVM_API int cvm_ctx_set_profiling(cvm_ctx* ctx, int enabled);
+CVM_API int cvm_ctx_kernel_stats(cvm_ctx* ctx, cvm_kernel_stats* out);
+CVM_API int cvm_ctx_reset_stats(cvm_ctx* ctx);
+/* Device-resident scratch write larger than L2 (for cold-cache timing). */
+CVM_API int cvm_ctx_flush_l2(cvm_ctx* ctx);
+/* Time a region on the context stream with CUDA events. */
+CVM_API int cvm_ctx_event_record(cvm_ctx* ctx, int which);  /* 0 start, 1 stop */
+CVM_API int cvm_ctx_event_elapsed_ms(cvm_ctx* ctx, double* ms);
+/* Measured FP64 FMA-pipe peak of this device in TFLOP/s (roofline denominator
+ * of the blind-rotation kernel) and its SM count. */
+CVM_API int cvm_ctx_fp64_peak(cvm_ctx* ctx, int reps, double* tflops);
+CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
+
+/* ------------------------------------------------------------------------
+ * Backend: the cryptovm::Backend contract (gates.hpp:109-132) over a context.
+ * Gate calls return handles immediately (lazy recording); evaluation happens
+ * in dataflow levels at flush points: decrypt/export, or cvm_backend_flush.
+ * Handles are dense 1-based node ids like the reference's GateDag
+ * (dag.cpp:57-73); 0 is the invalid handle (BitHandle::valid(), gates.hpp:95).
+ * ---------------------------------------------------------------------- */
+typedef struct cvm_backend cvm_backend;
+typedef uint64_t cvm_handle;
+CVM_API int cvm_backend_create(cvm_ctx* ctx, const cvm_keyset* owner,
+                               uint64_t enc_seed, cvm_backend** out);
+CVM_API void cvm_backend_destroy(cvm_backend* b);
+CVM_API int cvm_backend_constant(cvm_backend* b, int value, cvm_handle* out);
+CVM_API int cvm_backend_unary_gate(cvm_backend* b, uint32_t kind, cvm_handle a,
+                                   cvm_handle* out);
+CVM_API int cvm_backend_binary_gate(cvm_backend* b, uint32_t kind, cvm_handle a,
+                                    cvm_handle c, cvm_handle* out);
+CVM_API int cvm_backend_mux_gate(cvm_backend* b, cvm_handle sel, cvm_handle on_true,
+                                 cvm_handle on_false, cvm_handle* out);
+CVM_API int cvm_backend_encrypt_bit(cvm_backend* b, int value, cvm_handle* out);
+CVM_API int cvm_backend_decrypt_bit(cvm_backend* b, cvm_handle h, int* value);
+/* Batched key-owner decryption: one flush, one download. */
+CVM_API int cvm_backend_decrypt_bits(cvm_backend* b, size_t count,
+                                     const cvm_handle* hs, uint8_t* values);
+/* Import existing ciphertexts (631 u32 each) as fresh input handles. */
+CVM_API int cvm_backend_import_lwe(cvm_backend* b, size_t count,
+                                   const uint32_t* lwe, cvm_handle* out);
+CVM_API int cvm_backend_export_lwe(cvm_backend* b, size_t count,
+                                   const cvm_handle* hs, uint32_t* lwe);
+/* export_bit / import_bit: 2,524-byte little-endian blob (631 x u32). */
+CVM_API int cvm_backend_export_bit(cvm_backend* b, cvm_handle h, uint8_t* blob,
+                                   size_t blob_size);
+CVM_API int cvm_backend_import_bit(cvm_backend* b, const uint8_t* blob,
+                                   size_t blob_size, cvm_handle* out);
+CVM_API int cvm_backend_push_region(cvm_backend* b, const char* name);
+CVM_API int cvm_backend_pop_region(cvm_backend* b);
+CVM_API int cvm_backend_fence(cvm_backend* b);
+CVM_API int cvm_backend_flush(cvm_backend* b);
+
+typedef struct cvm_backend_stats {
+  uint64_t nodes, bootstrapped, bootstraps, levels_run, flushes, decrypts;
+  uint64_t last_flush_levels, last_flush_gates, max_level_width;
+} cvm_backend_stats;
+CVM_API int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out);
+/* Node table: kind, input flag, deps (0 = none), constant value per node id. */
+CVM_API int cvm_backend_node_count(const cvm_backend* b, uint64_t* out);
+CVM_API int cvm_backend_nodes(const cvm_backend* b, uint64_t first, uint64_t count,
+                              int64_t* rows /* count x 7 */);
+
+/* ------------------------------------------------------------------------
+ * Functional units (reference alu.hpp:68-136), emitting gates into a backend.
+ * Words are arrays of `width` handles, LSB first (word.hpp:28-57).
+ * ---------------------------------------------------------------------- */
+typedef enum cvm_fu_op {
+  CVM_FU_ADD = 0,       /* alu::add               out: width + carry      */
+  CVM_FU_ADD_CIN = 1,   /* alu::add(carry_in = c[0])                      */
+  CVM_FU_SUB = 2,       /* alu::sub               out: width + carry      */
+  CVM_FU_ADDSUB = 3,    /* alu::add_sub_select(subtract = c[0])           */
+  CVM_FU_CMP = 4,       /* SUBS/CMP: sub + flags  out: width + N,Z,C,V    */
+  CVM_FU_AND = 5, CVM_FU_ORR = 6, CVM_FU_EOR = 7, CVM_FU_ORN = 8,
+  CVM_FU_LSL = 9, CVM_FU_LSR = 10, CVM_FU_ASR = 11, /* shift_reg by word b */
+  CVM_FU_UMUL = 12,     /* alu::mul_unsigned      out: 2*width            */
+  CVM_FU_SMUL = 13,     /* alu::mul_signed        out: 2*width            */
+  CVM_FU_UDIV = 14,     /* alu::div_unsigned (Widened) out: width         */
+  CVM_FU_UDIV_EXACT = 15
+} cvm_fu_op;
+CVM_API int cvm_fu_out_width(uint32_t op, uint32_t width);
+CVM_API int cvm_fu_apply(cvm_backend* b, uint32_t op, uint32_t width,
+                         const cvm_handle* a, const cvm_handle* bw,
+                         const cvm_handle* c, cvm_handle* out);
+
+/* Batched FU evaluation through the public path (host buffers in and out):
+ * `batch` independent instances; operands a, b (and c for ADD_CIN/ADDSUB) are
+ * ciphertexts batch x width x 631 u32 (c: batch x 631); results batch x
+ * out_width x 631.  Records the circuits on a fresh backend, flushes the
+ * levelised DAG through the device, downloads the outputs. */
+CVM_API int cvm_fu_batch(cvm_ctx* ctx, uint32_t op, uint32_t width, uint64_t batch,
+                         const uint32_t* a_lwe, const uint32_t* b_lwe,
+                         const uint32_t* c_lwe, uint32_t* out_lwe,
+                         cvm_backend_stats* stats);
+
+/* ------------------------------------------------------------------------
+ * Emulator (reference Machine, emulator.hpp:87-133) for straight-line
+ * programs: LOAD/STORE/MOV/ADD(S)/SUB(S)/MUL(S)/SMUL(S)/UDIV/LLS/LRS/ARS/AND/
+ * OR/XOR/ORN/NOT/BFC/BFI/RBIT/REV/CMP/HALT (register or immediate operands;
+ * B is rejected: it needs the key owner's branch oracle); fence after every
+ * instruction is recorded but scheduling follows dataflow.
+ * ---------------------------------------------------------------------- */
+typedef struct cvm_insn {
+  uint32_t op;        /* cryptovm::Opcode enumerator (isa.hpp:27-55)      */
+  int32_t rd, rn, rm; /* -1 = absent                                     */
+  int64_t imm;        /* -1 = absent                                     */
+  int64_t imm2;       /* BFC/BFI field width, -1 = absent                */
+  int32_t sets_flags;
+  int32_t pad;
+} cvm_insn;
+CVM_API int cvm_machine_run(cvm_backend* b, uint32_t word_size,
+                            uint32_t register_count, const cvm_handle* memory,
+                            uint32_t memory_words, const cvm_insn* program,
+                            uint32_t count, cvm_handle* regs_out,
+                            cvm_handle* nzcv_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CVM_GPU_H_ */

@@ -1,0 +1,290 @@
+// GpuBackend: the cryptovm::Backend contract (gates.hpp:109-132) over the
+// device context, with lazy recording and dataflow levelisation.
+//
+// Reference behaviour kept:
+//  * every gate call returns a handle immediately; handles are dense 1-based
+//    node ids as in GateDag::append (dag.cpp:57-73), 0 is invalid;
+//  * invalid handles / wrong kinds raise InputError before anything is
+//    enqueued (sim_backend.cpp:47-57,80-83);
+//  * CONSTANT, NOT and COPY are not bootstrapped (gates.cpp:35-50): here they
+//    are folded into a linear form (sign * slot + constant) consumed by the
+//    next bootstrapped gate's input combination, so they cost nothing;
+//  * regions and fences are recorded, but a fence is only a latency-model
+//    annotation (dag.hpp:44-48): gates are pure, so evaluation
+//    follows dataflow -- the level of a gate is 1 + the deepest level among
+//    its not-yet-evaluated inputs.
+// Evaluation happens at flush points (decrypt / export / explicit flush):
+// each pending level becomes one cvm_submit_level (two launches).
+#include <algorithm>
+#include <cstring>
+
+#include "cvm_internal.hpp"
+
+namespace cvm {
+
+int bootstrap_count(GateKind k) {
+  switch (k) {
+    case GateKind::Constant:
+    case GateKind::Not:
+    case GateKind::Copy:
+      return 0;
+    case GateKind::Mux:
+      return 2;
+    default:
+      return 1;
+  }
+}
+
+GpuBackend::GpuBackend(Context* ctx, const KeySet* owner, uint64_t enc_seed)
+    : ctx_(ctx), owner_(owner), enc_seed_(enc_seed) {
+  if (!ctx_) throw InputError("backend needs a device context");
+  if (!context_has_keys(ctx_)) throw StateError("upload keys before creating a backend");
+  nodes_.reserve(1 << 16);
+}
+
+const Node& GpuBackend::node(Bit h, const char* what) const {
+  if (h == 0 || h > nodes_.size())
+    throw InputError(std::string("invalid bit handle passed to ") + what);
+  return nodes_[h - 1];
+}
+
+Bit GpuBackend::add_node(Node n) {
+  nodes_.push_back(n);
+  stats_.nodes = nodes_.size();
+  return nodes_.size();
+}
+
+cvm_operand GpuBackend::operand(Bit h) const {
+  const Node& n = nodes_[h - 1];
+  return cvm_operand{n.slot, n.sign, n.constant};
+}
+
+Bit GpuBackend::constant(bool value) {
+  std::lock_guard<std::mutex> lock(mu_);
+  Node n{};
+  n.kind = GateKind::Constant;
+  n.const_value = value;
+  n.slot = -1;
+  n.sign = 1;
+  n.constant = value ? kMu : 0u - kMu;  // trivial sample (0, +-1/8)
+  return add_node(n);
+}
+
+Bit GpuBackend::unary_gate(GateKind kind, Bit a) {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (kind != GateKind::Not && kind != GateKind::Copy)
+    throw InputError("not a unary gate");
+  const Node& in = node(a, "unary_gate");
+  Node n = in;
+  n.kind = kind;
+  n.input = false;
+  n.const_value = false;
+  n.ndeps = 1;
+  n.dep[0] = a;
+  n.dep[1] = n.dep[2] = 0;
+  if (kind == GateKind::Not) {
+    n.sign = -in.sign;
+    n.constant = 0u - in.constant;
+  }
+  return add_node(n);
+}
+
+Bit GpuBackend::binary_gate(GateKind kind, Bit a, Bit b) {
+  std::lock_guard<std::mutex> lock(mu_);
+  const Node& na = node(a, "binary_gate");
+  const Node& nb = node(b, "binary_gate");
+  if (bootstrap_count(kind) != 1) throw InputError("not a bootstrapped binary gate");
+  Node n{};
+  n.kind = kind;
+  n.ndeps = 2;
+  n.dep[0] = a;
+  n.dep[1] = b;
+  n.level = std::max(na.level, nb.level) + 1;
+  n.slot = int64_t(take_slot());
+  n.sign = 1;
+  n.constant = 0;
+  cvm_gate g{};
+  g.kind = uint32_t(kind);
+  g.in[0] = operand(a);
+  g.in[1] = operand(b);
+  g.in[2] = cvm_operand{-1, 1, 0};
+  g.out_slot = uint64_t(n.slot);
+  if (pending_levels_.size() < n.level) pending_levels_.resize(n.level);
+  pending_levels_[n.level - 1].push_back(g);
+  stats_.bootstrapped++;
+  stats_.bootstraps++;
+  return add_node(n);
+}
+
+Bit GpuBackend::mux_gate(Bit sel, Bit on_true, Bit on_false) {
+  std::lock_guard<std::mutex> lock(mu_);
+  const Node& ns = node(sel, "mux_gate");
+  const Node& nt = node(on_true, "mux_gate");
+  const Node& nf = node(on_false, "mux_gate");
+  Node n{};
+  n.kind = GateKind::Mux;
+  n.ndeps = 3;
+  n.dep[0] = sel;
+  n.dep[1] = on_true;
+  n.dep[2] = on_false;
+  n.level = std::max({ns.level, nt.level, nf.level}) + 1;
+  n.slot = int64_t(take_slot());
+  n.sign = 1;
+  cvm_gate g{};
+  g.kind = uint32_t(GateKind::Mux);
+  g.in[0] = operand(sel);
+  g.in[1] = operand(on_true);
+  g.in[2] = operand(on_false);
+  g.out_slot = uint64_t(n.slot);
+  if (pending_levels_.size() < n.level) pending_levels_.resize(n.level);
+  pending_levels_[n.level - 1].push_back(g);
+  stats_.bootstrapped++;
+  stats_.bootstraps += 2;
+  return add_node(n);
+}
+
+Bit GpuBackend::encrypt_bit(bool value) {
+  if (!owner_) throw StateError("encrypt_bit needs the key owner's keyset");
+  uint32_t c[kLweWords];
+  const uint8_t bit = value ? 1 : 0;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    owner_->encrypt(enc_seed_ * 0x9E3779B97F4A7C15ull + enc_counter_++, 1, &bit, c);
+  }
+  Bit h;
+  import_lwe(1, c, &h);
+  return h;
+}
+
+void GpuBackend::import_lwe(size_t count, const uint32_t* lwe, Bit* out) {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (count && !lwe) throw InputError("import: null ciphertexts");
+  for (size_t i = 0; i < count; ++i) {
+    const uint64_t s = take_slot();
+    // Staged uploads form one contiguous slot run; start a new run otherwise.
+    if (!pending_upload_.empty() &&
+        pending_upload_slot_ + pending_upload_.size() / kLweWords != s)
+      stage_uploads();
+    if (pending_upload_.empty()) pending_upload_slot_ = s;
+    pending_upload_.insert(pending_upload_.end(), lwe + i * kLweWords,
+                           lwe + (i + 1) * kLweWords);
+    Node n{};
+    n.kind = GateKind::Constant;
+    n.input = true;
+    n.slot = int64_t(s);
+    n.sign = 1;
+    out[i] = add_node(n);
+  }
+}
+
+uint64_t GpuBackend::take_slot() {
+  if (next_slot_ == chunk_end_) {
+    next_slot_ = context_alloc_slots(ctx_, chunk_);
+    chunk_end_ = next_slot_ + chunk_;
+    chunk_ = std::min<uint64_t>(chunk_ * 2, uint64_t(1) << 20);
+  }
+  return next_slot_++;
+}
+
+// Copies the staged run into pinned memory and enqueues its upload.
+void GpuBackend::stage_uploads() {
+  if (pending_upload_.empty()) return;
+  context_reserve(ctx_, context_slots_used(ctx_));
+  context_upload(ctx_, pending_upload_slot_, pending_upload_.size() / kLweWords,
+                 pending_upload_.data());
+  pending_upload_.clear();
+}
+
+void GpuBackend::flush() {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (pending_upload_.empty() && pending_levels_.empty()) return;
+  context_reserve(ctx_, context_slots_used(ctx_));
+  stage_uploads();
+  uint64_t gates = 0;
+  for (const auto& lv : pending_levels_) {
+    context_submit_level(ctx_, lv.data(), lv.size());
+    gates += lv.size();
+    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, lv.size());
+  }
+  context_sync(ctx_);
+  stats_.flushes++;
+  stats_.levels_run += pending_levels_.size();
+  stats_.last_flush_levels = pending_levels_.size();
+  stats_.last_flush_gates = gates;
+  pending_upload_.clear();
+  pending_levels_.clear();
+  for (Node& n : nodes_) n.level = 0;  // everything is now resident
+}
+
+void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
+  for (size_t i = 0; i < count; ++i) node(hs[i], "export");
+  flush();
+  std::lock_guard<std::mutex> lock(mu_);
+  // Download the covering slot range in runs, then apply the linear forms.
+  std::vector<int64_t> slots;
+  for (size_t i = 0; i < count; ++i)
+    if (nodes_[hs[i] - 1].slot >= 0) slots.push_back(nodes_[hs[i] - 1].slot);
+  std::sort(slots.begin(), slots.end());
+  slots.erase(std::unique(slots.begin(), slots.end()), slots.end());
+  std::vector<uint32_t> buf;
+  std::vector<std::pair<int64_t, size_t>> where;  // slot -> offset in buf
+  size_t i = 0;
+  while (i < slots.size()) {
+    size_t j = i;
+    while (j + 1 < slots.size() && slots[j + 1] - slots[j] <= 16) ++j;
+    const uint64_t lo = uint64_t(slots[i]), n = uint64_t(slots[j] - slots[i] + 1);
+    const size_t off = buf.size();
+    buf.resize(off + n * kLweWords);
+    context_download(ctx_, lo, n, buf.data() + off);
+    for (size_t k = i; k <= j; ++k)
+      where.push_back({slots[k], off + size_t(slots[k] - slots[i]) * kLweWords});
+    i = j + 1;
+  }
+  for (size_t q = 0; q < count; ++q) {
+    const Node& n = nodes_[hs[q] - 1];
+    uint32_t* o = out + q * kLweWords;
+    if (n.slot < 0) {
+      std::memset(o, 0, kLweWords * 4);
+    } else {
+      auto it = std::lower_bound(where.begin(), where.end(), std::make_pair(n.slot, size_t(0)));
+      const uint32_t* src = buf.data() + it->second;
+      for (int w = 0; w < kLweWords; ++w) o[w] = n.sign > 0 ? src[w] : 0u - src[w];
+    }
+    o[kN] += n.constant;
+  }
+}
+
+bool GpuBackend::decrypt_bit(Bit bit) {
+  uint8_t v;
+  decrypt_bits(1, &bit, &v);
+  return v != 0;
+}
+
+void GpuBackend::decrypt_bits(size_t count, const Bit* hs, uint8_t* out) {
+  if (!owner_) throw StateError("decrypt needs the key owner's keyset");
+  std::vector<uint32_t> c(count * kLweWords);
+  export_lwe(count, hs, c.data());
+  for (size_t i = 0; i < count; ++i) out[i] = owner_->decrypt(&c[i * kLweWords]) ? 1 : 0;
+  std::lock_guard<std::mutex> lock(mu_);
+  stats_.decrypts += count;
+}
+
+void GpuBackend::push_region(std::string_view name) {
+  std::lock_guard<std::mutex> lock(mu_);
+  regions_.emplace_back(name);
+}
+
+void GpuBackend::pop_region() {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (regions_.empty()) throw InputError("pop_region without a matching push_region");
+  regions_.pop_back();
+}
+
+void GpuBackend::fence() {
+  std::lock_guard<std::mutex> lock(mu_);
+  ++fences_;
+}
+
+cvm_backend_stats GpuBackend::stats() const { return stats_; }
+
+}  // namespace cvm

@@ -1,0 +1,480 @@
+// extern "C" wrappers (include/cvm_gpu.h).  Exceptions become status codes
+// and a thread-local message, mirroring the reference's InputError / Error
+// split (errors.hpp:24-58).
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "cvm_internal.hpp"
+
+using namespace cvm;
+
+struct cvm_keyset {
+  KeySet ks;
+  explicit cvm_keyset(uint64_t seed) : ks(seed) {}
+};
+struct cvm_ctx {
+  Context* ctx;
+  uint64_t enc_seed = 1;
+};
+struct cvm_backend {
+  std::unique_ptr<Backend> impl;
+  GpuBackend* gpu = nullptr;      // set for the device backend
+  ClearBackend* clear = nullptr;  // set for the cleartext recorder
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return CVM_OK;
+  } catch (const InputError& e) {
+    g_err = e.what();
+    return CVM_E_INPUT;
+  } catch (const StateError& e) {
+    g_err = e.what();
+    return CVM_E_STATE;
+  } catch (const DeviceError& e) {
+    g_err = e.what();
+    return CVM_E_DEVICE;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return CVM_E_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CVM_E_DEVICE;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw InputError(std::string("null ") + what);
+}
+
+GateKind kind_of(uint32_t k) {
+  if (k > uint32_t(GateKind::Mux)) throw InputError("unknown gate kind " + std::to_string(k));
+  return GateKind(k);
+}
+
+Word to_word(const cvm_handle* h, uint32_t w) { return Word(h, h + w); }
+
+}  // namespace
+
+extern "C" {
+
+const char* cvm_last_error(void) { return g_err.c_str(); }
+const char* cvm_version(void) { return "cvm_b200 0.1 (sm_100a, FP64-FFT blind rotation)"; }
+
+// ------------------------------------------------------------- key owner --
+int cvm_keyset_generate(uint64_t seed, cvm_keyset** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new cvm_keyset(seed);
+  });
+}
+void cvm_keyset_destroy(cvm_keyset* ks) { delete ks; }
+int cvm_keyset_export(const cvm_keyset* k, int32_t* lwe_key, int32_t* tlwe_key, uint32_t* bk,
+                      uint32_t* ksk) {
+  return guard([&] {
+    need(k, "keyset");
+    if (lwe_key) std::memcpy(lwe_key, k->ks.lwe_key.data(), kN * 4);
+    if (tlwe_key) std::memcpy(tlwe_key, k->ks.tlwe_key.data(), kPolyN * 4);
+    if (bk) std::memcpy(bk, k->ks.bk.data(), kBkWords * 4);
+    if (ksk) std::memcpy(ksk, k->ks.ksk.data(), kKskWords * 4);
+  });
+}
+int cvm_encrypt_bits(const cvm_keyset* k, uint64_t seed, size_t count, const uint8_t* bits,
+                     uint32_t* out) {
+  return guard([&] {
+    need(k, "keyset");
+    if (count) {
+      need(bits, "bits");
+      need(out, "out");
+    }
+    k->ks.encrypt(seed, count, bits, out);
+  });
+}
+int cvm_decrypt_bits(const cvm_keyset* k, size_t count, const uint32_t* lwe, uint8_t* bits,
+                     int32_t* phases) {
+  return guard([&] {
+    need(k, "keyset");
+    if (count) need(lwe, "lwe");
+    for (size_t i = 0; i < count; ++i) {
+      const int32_t ph = k->ks.phase(lwe + i * kLweWords);
+      if (bits) bits[i] = ph > 0;
+      if (phases) phases[i] = ph;
+    }
+  });
+}
+
+// ----------------------------------------------------------- device ctx --
+int cvm_ctx_create(int device, cvm_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new cvm_ctx{context_create(device)};
+  });
+}
+void cvm_ctx_destroy(cvm_ctx* c) {
+  if (!c) return;
+  context_destroy(c->ctx);
+  delete c;
+}
+int cvm_upload_keys(cvm_ctx* c, const uint32_t* bk, const uint32_t* ksk) {
+  return guard([&] {
+    need(c, "ctx");
+    context_upload_keys(c->ctx, bk, ksk);
+  });
+}
+int cvm_upload_keyset(cvm_ctx* c, const cvm_keyset* k) {
+  return guard([&] {
+    need(c, "ctx");
+    need(k, "keyset");
+    context_upload_keys(c->ctx, k->ks.bk.data(), k->ks.ksk.data());
+  });
+}
+int cvm_slots_reserve(cvm_ctx* c, uint64_t n) {
+  return guard([&] {
+    need(c, "ctx");
+    context_reserve(c->ctx, n);
+  });
+}
+int cvm_slots_alloc(cvm_ctx* c, uint64_t n, uint64_t* first) {
+  return guard([&] {
+    need(c, "ctx");
+    need(first, "first");
+    *first = context_alloc_slots(c->ctx, n);
+    context_reserve(c->ctx, context_slots_used(c->ctx));
+  });
+}
+uint64_t cvm_slots_capacity(const cvm_ctx* c) { return c ? context_capacity(c->ctx) : 0; }
+int cvm_upload_lwe(cvm_ctx* c, uint64_t slot, uint64_t count, const uint32_t* lwe) {
+  return guard([&] {
+    need(c, "ctx");
+    context_upload(c->ctx, slot, count, lwe);
+  });
+}
+int cvm_download_lwe(cvm_ctx* c, uint64_t slot, uint64_t count, uint32_t* lwe) {
+  return guard([&] {
+    need(c, "ctx");
+    context_download(c->ctx, slot, count, lwe);
+  });
+}
+int cvm_submit_level(cvm_ctx* c, const cvm_gate* gates, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    context_submit_level(c->ctx, gates, count);
+  });
+}
+int cvm_sync(cvm_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    context_sync(c->ctx);
+  });
+}
+int cvm_ctx_set_profiling(cvm_ctx* c, int on) {
+  return guard([&] {
+    need(c, "ctx");
+    context_set_profiling(c->ctx, on != 0);
+  });
+}
+int cvm_ctx_kernel_stats(cvm_ctx* c, cvm_kernel_stats* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = context_stats(c->ctx);
+  });
+}
+int cvm_ctx_reset_stats(cvm_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    context_reset_stats(c->ctx);
+  });
+}
+int cvm_ctx_flush_l2(cvm_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    context_flush_l2(c->ctx);
+  });
+}
+int cvm_ctx_event_record(cvm_ctx* c, int which) {
+  return guard([&] {
+    need(c, "ctx");
+    context_event(c->ctx, which);
+  });
+}
+int cvm_ctx_event_elapsed_ms(cvm_ctx* c, double* ms) {
+  return guard([&] {
+    need(c, "ctx");
+    need(ms, "ms");
+    *ms = context_event_elapsed(c->ctx);
+  });
+}
+
+int cvm_ctx_fp64_peak(cvm_ctx* c, int reps, double* tflops) {
+  return guard([&] {
+    need(c, "ctx");
+    need(tflops, "tflops");
+    *tflops = context_fp64_peak(c->ctx, reps < 1 ? 1 : reps);
+  });
+}
+int cvm_ctx_sm_count(cvm_ctx* c, int* sms) {
+  return guard([&] {
+    need(c, "ctx");
+    need(sms, "sms");
+    *sms = context_sm_count(c->ctx);
+  });
+}
+
+// -------------------------------------------------------------- backend --
+int cvm_backend_create(cvm_ctx* c, const cvm_keyset* owner, uint64_t enc_seed,
+                       cvm_backend** out) {
+  return guard([&] {
+    need(out, "out");
+    auto b = std::make_unique<cvm_backend>();
+    if (c) {
+      auto g = std::make_unique<GpuBackend>(c->ctx, owner ? &owner->ks : nullptr, enc_seed);
+      b->gpu = g.get();
+      b->impl = std::move(g);
+    } else {
+      auto r = std::make_unique<ClearBackend>();
+      b->clear = r.get();
+      b->impl = std::move(r);
+    }
+    *out = b.release();
+  });
+}
+void cvm_backend_destroy(cvm_backend* b) { delete b; }
+int cvm_backend_constant(cvm_backend* b, int v, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->impl->constant(v != 0);
+  });
+}
+int cvm_backend_unary_gate(cvm_backend* b, uint32_t kind, cvm_handle a, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->impl->unary_gate(kind_of(kind), a);
+  });
+}
+int cvm_backend_binary_gate(cvm_backend* b, uint32_t kind, cvm_handle x, cvm_handle y,
+                            cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->impl->binary_gate(kind_of(kind), x, y);
+  });
+}
+int cvm_backend_mux_gate(cvm_backend* b, cvm_handle s, cvm_handle t, cvm_handle f,
+                         cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->impl->mux_gate(s, t, f);
+  });
+}
+int cvm_backend_encrypt_bit(cvm_backend* b, int v, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->impl->encrypt_bit(v != 0);
+  });
+}
+int cvm_backend_decrypt_bit(cvm_backend* b, cvm_handle h, int* v) {
+  return guard([&] {
+    need(b, "backend");
+    need(v, "out");
+    *v = b->impl->decrypt_bit(h) ? 1 : 0;
+  });
+}
+int cvm_backend_decrypt_bits(cvm_backend* b, size_t n, const cvm_handle* hs, uint8_t* out) {
+  return guard([&] {
+    need(b, "backend");
+    if (n) {
+      need(hs, "handles");
+      need(out, "out");
+    }
+    if (b->gpu) b->gpu->decrypt_bits(n, hs, out);
+    else
+      for (size_t i = 0; i < n; ++i) out[i] = b->impl->decrypt_bit(hs[i]) ? 1 : 0;
+  });
+}
+int cvm_backend_import_lwe(cvm_backend* b, size_t n, const uint32_t* lwe, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    if (!b->gpu) throw InputError("the cleartext recorder holds no ciphertexts");
+    if (n) need(out, "out");
+    b->gpu->import_lwe(n, lwe, out);
+  });
+}
+int cvm_backend_export_lwe(cvm_backend* b, size_t n, const cvm_handle* hs, uint32_t* lwe) {
+  return guard([&] {
+    need(b, "backend");
+    if (!b->gpu) throw InputError("the cleartext recorder holds no ciphertexts");
+    if (n) {
+      need(hs, "handles");
+      need(lwe, "out");
+    }
+    b->gpu->export_lwe(n, hs, lwe);
+  });
+}
+int cvm_backend_export_bit(cvm_backend* b, cvm_handle h, uint8_t* blob, size_t size) {
+  return guard([&] {
+    need(b, "backend");
+    need(blob, "blob");
+    if (size != kLweWords * 4) throw InputError("bit ciphertexts are 2524-byte blobs");
+    if (!b->gpu) throw InputError("the cleartext recorder holds no ciphertexts");
+    uint32_t c[kLweWords];
+    b->gpu->export_lwe(1, &h, c);
+    std::memcpy(blob, c, sizeof(c));  // little-endian host
+  });
+}
+int cvm_backend_import_bit(cvm_backend* b, const uint8_t* blob, size_t size, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(blob, "blob");
+    need(out, "out");
+    if (size != kLweWords * 4) throw InputError("bit ciphertexts are 2524-byte blobs");
+    if (!b->gpu) throw InputError("the cleartext recorder holds no ciphertexts");
+    uint32_t c[kLweWords];
+    std::memcpy(c, blob, sizeof(c));
+    b->gpu->import_lwe(1, c, out);
+  });
+}
+int cvm_backend_push_region(cvm_backend* b, const char* name) {
+  return guard([&] {
+    need(b, "backend");
+    need(name, "name");
+    b->impl->push_region(name);
+  });
+}
+int cvm_backend_pop_region(cvm_backend* b) {
+  return guard([&] {
+    need(b, "backend");
+    b->impl->pop_region();
+  });
+}
+int cvm_backend_fence(cvm_backend* b) {
+  return guard([&] {
+    need(b, "backend");
+    b->impl->fence();
+  });
+}
+int cvm_backend_flush(cvm_backend* b) {
+  return guard([&] {
+    need(b, "backend");
+    if (b->gpu) b->gpu->flush();
+  });
+}
+int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->gpu ? b->gpu->stats() : b->clear->stats();
+  });
+}
+int cvm_backend_node_count(const cvm_backend* b, uint64_t* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    *out = b->gpu ? b->gpu->nodes().size() : b->clear->nodes().size();
+  });
+}
+int cvm_backend_nodes(const cvm_backend* b, uint64_t first, uint64_t count, int64_t* rows) {
+  return guard([&] {
+    need(b, "backend");
+    const std::vector<Node>& ns = b->gpu ? b->gpu->nodes() : b->clear->nodes();
+    if (first + count > ns.size()) throw InputError("node range out of bounds");
+    if (count) need(rows, "rows");
+    for (uint64_t i = 0; i < count; ++i) {
+      const Node& n = ns[first + i];
+      int64_t* r = rows + i * 7;
+      r[0] = int64_t(n.kind);
+      r[1] = n.input;
+      r[2] = n.ndeps;
+      r[3] = int64_t(n.dep[0]);
+      r[4] = int64_t(n.dep[1]);
+      r[5] = int64_t(n.dep[2]);
+      r[6] = n.const_value;
+    }
+  });
+}
+
+// ----------------------------------------------------- functional units --
+int cvm_fu_out_width(uint32_t op, uint32_t width) { return fu_out_width(op, width); }
+
+int cvm_fu_apply(cvm_backend* b, uint32_t op, uint32_t width, const cvm_handle* a,
+                 const cvm_handle* bw, const cvm_handle* c, cvm_handle* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(a, "a");
+    need(bw, "b");
+    need(out, "out");
+    const int ow = fu_out_width(op, width);
+    if (ow < 0) throw InputError("unknown functional-unit op");
+    const bool uses_c = op == CVM_FU_ADD_CIN || op == CVM_FU_ADDSUB;
+    if (uses_c) need(c, "c");
+    Word r = fu_apply(*b->impl, op, to_word(a, width), to_word(bw, width), uses_c ? *c : 0);
+    std::memcpy(out, r.data(), r.size() * sizeof(Bit));
+  });
+}
+
+int cvm_fu_batch(cvm_ctx* c, uint32_t op, uint32_t width, uint64_t batch, const uint32_t* a_lwe,
+                 const uint32_t* b_lwe, const uint32_t* c_lwe, uint32_t* out_lwe,
+                 cvm_backend_stats* stats) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a_lwe, "a");
+    need(b_lwe, "b");
+    need(out_lwe, "out");
+    const int ow = fu_out_width(op, width);
+    if (ow < 0) throw InputError("unknown functional-unit op");
+    const bool uses_c = op == CVM_FU_ADD_CIN || op == CVM_FU_ADDSUB;
+    if (uses_c) need(c_lwe, "c");
+    GpuBackend bk(c->ctx, nullptr, 0);
+    std::vector<Bit> ha(batch * width), hb(batch * width), hc(uses_c ? batch : 0);
+    bk.import_lwe(ha.size(), a_lwe, ha.data());
+    bk.import_lwe(hb.size(), b_lwe, hb.data());
+    if (uses_c) bk.import_lwe(hc.size(), c_lwe, hc.data());
+    std::vector<Bit> outs;
+    outs.reserve(batch * size_t(ow));
+    for (uint64_t i = 0; i < batch; ++i) {
+      Word r = fu_apply(bk, op, Word(&ha[i * width], &ha[i * width] + width),
+                        Word(&hb[i * width], &hb[i * width] + width), uses_c ? hc[i] : 0);
+      outs.insert(outs.end(), r.begin(), r.end());
+    }
+    bk.export_lwe(outs.size(), outs.data(), out_lwe);
+    if (stats) *stats = bk.stats();
+  });
+}
+
+// -------------------------------------------------------------- machine --
+int cvm_machine_run(cvm_backend* b, uint32_t word_size, uint32_t register_count,
+                    const cvm_handle* memory, uint32_t memory_words, const cvm_insn* program,
+                    uint32_t count, cvm_handle* regs_out, cvm_handle* nzcv_out) {
+  return guard([&] {
+    need(b, "backend");
+    if (count) need(program, "program");
+    std::vector<Word> mem;
+    for (uint32_t w = 0; w < memory_words; ++w)
+      mem.push_back(Word(memory + size_t(w) * word_size, memory + size_t(w + 1) * word_size));
+    std::vector<Word> regs;
+    alu::Flags f{};
+    machine_run(*b->impl, word_size, register_count, mem, program, count, &regs, &f);
+    if (regs_out)
+      for (size_t r = 0; r < regs.size(); ++r)
+        std::memcpy(regs_out + r * word_size, regs[r].data(), word_size * sizeof(Bit));
+    if (nzcv_out) {
+      nzcv_out[0] = f.n;
+      nzcv_out[1] = f.z;
+      nzcv_out[2] = f.c;
+      nzcv_out[3] = f.v;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+// Internal C++ interfaces behind the C ABI (include/cvm_gpu.h).
+#pragma once
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "../../include/cvm_gpu.h"
+#include "tfhe_params.h"
+
+namespace cvm {
+
+// Error taxonomy of the reference (errors.hpp:24-58): InputError for
+// precondition violations, Error for everything else (here: device failures).
+struct InputError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ------------------------------------------------------------- key owner --
+struct KeySet {
+  explicit KeySet(uint64_t seed);
+  void encrypt(uint64_t seed, size_t count, const uint8_t* bits, uint32_t* out) const;
+  int32_t phase(const uint32_t* lwe) const;
+  bool decrypt(const uint32_t* lwe) const { return phase(lwe) > 0; }
+
+  std::vector<int32_t> lwe_key, tlwe_key;
+  std::vector<uint32_t> bk, ksk;
+};
+
+// ------------------------------------------------------------ device ctx --
+class Context;
+Context* context_create(int device);
+void context_destroy(Context* c);
+void context_upload_keys(Context* c, const uint32_t* bk, const uint32_t* ksk);
+void context_reserve(Context* c, uint64_t n);
+uint64_t context_alloc_slots(Context* c, uint64_t n);  // returns first slot id
+uint64_t context_slots_used(const Context* c);
+uint64_t context_capacity(const Context* c);
+void context_upload(Context* c, uint64_t slot, uint64_t count, const uint32_t* lwe);
+void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe);
+void context_submit_level(Context* c, const cvm_gate* gates, uint64_t count);
+void context_sync(Context* c);
+bool context_has_keys(const Context* c);
+void context_set_profiling(Context* c, bool on);
+cvm_kernel_stats context_stats(Context* c);
+void context_reset_stats(Context* c);
+void context_flush_l2(Context* c);
+void context_event(Context* c, int which);
+double context_event_elapsed(Context* c);
+double context_fp64_peak(Context* c, int reps);
+int context_sm_count(const Context* c);
+
+// --------------------------------------------------------------- backend --
+// Mirror of cryptovm::Backend (gates.hpp:109-132) with handles as dense node
+// ids (0 = invalid), so the functional units below read like the reference.
+using Bit = uint64_t;
+using Word = std::vector<Bit>;
+
+enum class GateKind : uint8_t {
+  Constant, Not, Copy, Nand, And, Or, Xor, Xnor, Nor, AndNY, AndYN, OrNY, OrYN, Mux
+};
+int bootstrap_count(GateKind k);
+
+class Backend {
+ public:
+  virtual ~Backend() = default;
+  virtual Bit constant(bool value) = 0;
+  virtual Bit unary_gate(GateKind kind, Bit a) = 0;
+  virtual Bit binary_gate(GateKind kind, Bit a, Bit b) = 0;
+  virtual Bit mux_gate(Bit sel, Bit on_true, Bit on_false) = 0;
+  virtual Bit encrypt_bit(bool value) = 0;
+  virtual bool decrypt_bit(Bit bit) = 0;
+  virtual void push_region(std::string_view name) = 0;
+  virtual void pop_region() = 0;
+  virtual void fence() = 0;
+};
+
+inline Bit not_gate(Backend& b, Bit a) { return b.unary_gate(GateKind::Not, a); }
+inline Bit copy_gate(Backend& b, Bit a) { return b.unary_gate(GateKind::Copy, a); }
+inline Bit and_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::And, x, y); }
+inline Bit or_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Or, x, y); }
+inline Bit xor_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Xor, x, y); }
+inline Bit nand_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Nand, x, y); }
+
+class Region {  // RegionScope (gates.hpp:158-170)
+ public:
+  Region(Backend& b, std::string_view name) : b_(b) { b_.push_region(name); }
+  ~Region() { b_.pop_region(); }
+  Region(const Region&) = delete;
+  Region& operator=(const Region&) = delete;
+
+ private:
+  Backend& b_;
+};
+
+// Node record (the reference DagNode, dag.hpp:33-42, minus cost/region).
+struct Node {
+  GateKind kind;
+  bool input;
+  bool const_value;
+  uint8_t ndeps;
+  uint32_t level;       // dataflow level (bootstrapped depth), 0 = available
+  Bit dep[3];
+  // Linear form of the node's ciphertext: sign * slab[slot] + constant.
+  int64_t slot;         // -1: pure constant
+  int32_t sign;
+  uint32_t constant;
+};
+
+class GpuBackend final : public Backend {
+ public:
+  GpuBackend(Context* ctx, const KeySet* owner, uint64_t enc_seed);
+  Bit constant(bool value) override;
+  Bit unary_gate(GateKind kind, Bit a) override;
+  Bit binary_gate(GateKind kind, Bit a, Bit b) override;
+  Bit mux_gate(Bit sel, Bit on_true, Bit on_false) override;
+  Bit encrypt_bit(bool value) override;
+  bool decrypt_bit(Bit bit) override;
+  void push_region(std::string_view name) override;
+  void pop_region() override;
+  void fence() override;
+
+  void decrypt_bits(size_t n, const Bit* hs, uint8_t* out);
+  void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
+  void export_lwe(size_t n, const Bit* hs, uint32_t* out);
+  void flush();
+  cvm_backend_stats stats() const;
+  const std::vector<Node>& nodes() const { return nodes_; }
+
+ private:
+  const Node& node(Bit h, const char* what) const;
+  Bit add_node(Node n);
+  cvm_operand operand(Bit h) const;
+  uint64_t take_slot();
+  void stage_uploads();
+
+  std::mutex mu_;
+  Context* ctx_;
+  const KeySet* owner_;
+  uint64_t enc_seed_;
+  uint64_t enc_counter_ = 0;
+  std::vector<Node> nodes_;          // nodes_[id - 1]
+  uint64_t next_slot_ = 0, chunk_end_ = 0, chunk_ = 4096;  // slot chunk from ctx
+  // pending uploads (fresh encryptions / imports) and gates, by level
+  std::vector<uint32_t> pending_upload_;
+  uint64_t pending_upload_slot_ = 0;
+  std::vector<std::vector<cvm_gate>> pending_levels_;
+  std::vector<std::string> regions_;
+  uint64_t fences_ = 0;
+  cvm_backend_stats stats_{};
+};
+
+// Cleartext recorder: the SimBackend semantics (sim_backend.cpp:25-154) with
+// the same node table as GpuBackend.  It holds no ciphertexts and cannot run
+// the bootstrapping path; it exists so the host logic (circuits, levelisation,
+// DAG identity with the reference) is testable without a GPU, and as the
+// shadow that GPU results are checked against.
+class ClearBackend final : public Backend {
+ public:
+  Bit constant(bool value) override;
+  Bit unary_gate(GateKind kind, Bit a) override;
+  Bit binary_gate(GateKind kind, Bit a, Bit b) override;
+  Bit mux_gate(Bit sel, Bit on_true, Bit on_false) override;
+  Bit encrypt_bit(bool value) override;
+  bool decrypt_bit(Bit bit) override;
+  void push_region(std::string_view name) override;
+  void pop_region() override;
+  void fence() override;
+  cvm_backend_stats stats() const { return stats_; }
+  const std::vector<Node>& nodes() const { return nodes_; }
+
+ private:
+  Bit add(Node n, bool value);
+  bool value(Bit h, const char* what) const;
+  std::mutex mu_;
+  std::vector<Node> nodes_;
+  std::vector<uint8_t> values_;
+  size_t regions_ = 0;
+  cvm_backend_stats stats_{};
+};
+
+// ------------------------------------------------------ functional units --
+namespace alu {
+struct AddResult {
+  Word sum;
+  Bit carry_out;
+};
+struct Flags {
+  Bit n, z, c, v;
+};
+enum class ShiftKind { LogicalLeft, LogicalRight, ArithmeticRight };
+enum class BitwiseKind { And, Or, Xor, OrNot };
+enum class DivAccumulator { Widened, Exact };
+
+AddResult add(Backend& bk, const Word& a, const Word& b);
+AddResult add(Backend& bk, const Word& a, const Word& b, Bit carry_in);
+AddResult sub(Backend& bk, const Word& a, const Word& b);
+AddResult add_sub_select(Backend& bk, const Word& a, const Word& b, Bit subtract);
+Word shift_imm(Backend& bk, const Word& w, ShiftKind kind, unsigned amount);
+Word shift_reg(Backend& bk, const Word& w, ShiftKind kind, const Word& amount);
+Word mul_unsigned(Backend& bk, const Word& a, const Word& b);
+Word mul_signed(Backend& bk, const Word& a, const Word& b);
+Word div_unsigned(Backend& bk, const Word& n, const Word& d,
+                  DivAccumulator mode = DivAccumulator::Widened);
+Word bitwise(Backend& bk, BitwiseKind kind, const Word& a, const Word& b);
+Word not_word(Backend& bk, const Word& a);
+Word constant_word(Backend& bk, uint64_t value, unsigned width);
+Bit or_reduce(Backend& bk, const Word& w);
+Flags flags(Backend& bk, const Word& result, Bit carry_out, Bit a_msb, Bit b_msb);
+}  // namespace alu
+
+// Applies one cvm_fu_op; returns the output bits.
+Word fu_apply(Backend& bk, uint32_t op, const Word& a, const Word& b, Bit c);
+int fu_out_width(uint32_t op, uint32_t width);
+
+// Straight-line emulator (Machine, emulator.cpp:134-369).
+void machine_run(Backend& bk, unsigned word_size, unsigned register_count,
+                 const std::vector<Word>& memory, const cvm_insn* program,
+                 uint32_t count, std::vector<Word>* regs, alu::Flags* nzcv);
+
+}  // namespace cvm

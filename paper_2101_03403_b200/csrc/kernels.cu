@@ -1,0 +1,269 @@
+// sm_100a kernels of the batched TFHE gate-bootstrapping path.
+//
+//   bk_to_fft_kernel   K5  one-time: BK (time domain, u32) -> folded FFT domain,
+//                          pre-scaled by 1/M, in per-thread bin order.
+//   blind_rotate_kernel K1+K2 fused: gate-input combination + mod-switch
+//                          prologue, 630 CMux steps (gadget decomposition,
+//                          6 forward FFTs, 12 complex MACs against BK_i,
+//                          2 inverse FFTs, exact rounding), sample extraction.
+//   key_switch_kernel  K3+K4: (MUX combine) + LWE key switch N=1024 -> n=630.
+//
+// One CTA of 64 threads owns one bootstrap; the whole 630-step chain runs
+// inside one launch with the accumulator resident in shared memory.  See
+// DESIGN.md section 4 for the roofline of each kernel.
+#include <cuda_runtime.h>
+
+#include "fft512.cuh"
+#include "kernels.cuh"
+
+namespace cvm {
+
+// digits: buf = c + offset; d_p = ((buf >> (25 - 7p)) & 127) - 64
+constexpr uint32_t kDecompOffset =
+    (1u << (kBgBit - 1)) * ((1u << 25) + (1u << 18) + (1u << 11));
+constexpr double kDigitBias = 4503599627370496.0 + 64.0;  // 2^52 + Bg/2
+
+template <int kPattern>  // 1: fwd ex1, 2: fwd ex2 / inv exA, 3: inv exB
+__device__ __forceinline__ void exchange(c64 v[8], c64* buf, int t) {
+#pragma unroll
+  for (int z = 0; z < 8; ++z) {
+    int cell, slot;
+    if (kPattern == 1) {
+      cell = ex1_cell(t, z);
+      slot = t >> 3;
+    } else if (kPattern == 2) {
+      cell = ex2_cell(t, z);
+      slot = t >> 3;
+    } else {
+      cell = exB_cell(t, z);
+      slot = t & 7;
+    }
+    buf[xpos(cell, slot)] = v[z];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = buf[xpos(t, s)];
+}
+
+__device__ __forceinline__ c64 ldg_c64(const c64* p) {
+  double2 d = __ldg(reinterpret_cast<const double2*>(p));
+  return {d.x, d.y};
+}
+
+__device__ __forceinline__ void load_twiddles(const c64* tw1, const c64* tw2,
+                                              int t, c64 T1[8], c64 T2[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    T1[k] = ldg_c64(tw1 + t * 8 + k);
+    T2[k] = ldg_c64(tw2 + t * 8 + k);
+  }
+}
+
+// ----------------------------------------------------------------- K5 --
+__global__ void __launch_bounds__(64) bk_to_fft_kernel(const uint32_t* __restrict__ bk,
+                                                       const c64* __restrict__ tw1,
+                                                       const c64* __restrict__ tw2,
+                                                       c64* __restrict__ bkf) {
+  __shared__ c64 xbuf[2][512];
+  const int t = threadIdx.x;
+  const int poly = blockIdx.x;  // ((i*6 + row)*2 + o)
+  const int o = poly & 1, ir = poly >> 1;
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+  const uint32_t* p = bk + (size_t)poly * kPolyN;
+  c64 v[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+    v[a] = {(double)(int32_t)p[t + 64 * a], (double)(int32_t)p[t + 64 * a + 512]};
+  fwd_stage1(v, T1);
+  exchange<1>(v, xbuf[0], t);
+  fwd_stage2(v, T2);
+  exchange<2>(v, xbuf[1], t);
+  fwd_stage3(v);
+  const double s = 1.0 / kFftM;
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2)
+    bkf[((size_t)ir * 8 + k2) * 128 + t * 2 + o] = {v[k2].x * s, v[k2].y * s};
+}
+
+// ------------------------------------------------------------ K1 + K2 --
+__global__ void __launch_bounds__(64) blind_rotate_kernel(
+    const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
+    const c64* __restrict__ bkf, const c64* __restrict__ tw1,
+    const c64* __restrict__ tw2, uint32_t* __restrict__ xout) {
+  __shared__ uint32_t acc[2][kPolyN];
+  __shared__ c64 xbuf[2][512];
+  __shared__ uint16_t bar[kLweWords + 1];
+  const int t = threadIdx.x;
+  const BrJob job = jobs[blockIdx.x];
+
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+
+  // K1: combine the gate inputs and mod-switch to Z_2N.
+  for (int i = t; i < kLweWords; i += 64) {
+    uint32_t v = i == kN ? job.cst : 0u;
+    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
+    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
+    bar[i] = (uint16_t)modswitch_2n(v);
+  }
+  __syncthreads();
+  // ACC = X^{-barb} (0, mu * sum X^j)
+  {
+    const int barb = bar[kN];
+    for (int j = t; j < kPolyN; j += 64) {
+      acc[0][j] = 0;
+      acc[1][j] = (((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu);
+    }
+  }
+
+  for (int i = 0; i < kN; ++i) {
+    __syncthreads();
+    const int ai = bar[i];
+    if (ai == 0) continue;  // X^0 - 1 = 0: the CMux leaves ACC unchanged
+    const c64* bk_i = bkf + (size_t)i * kBkfComplexPerStep;
+    c64 af[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
+
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      // (X^{a_i} - 1) * ACC_part at the 16 coefficients this thread owns.
+      uint32_t dif[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = t + 64 * (q & 7) + (q >> 3) * 512;
+        const int m = (j - ai) & (2 * kPolyN - 1);
+        const uint32_t r = m < kPolyN ? acc[part][m] : 0u - acc[part][m - kPolyN];
+        dif[q] = r - acc[part][j] + kDecompOffset;
+      }
+#pragma unroll 1
+      for (int p = 0; p < kL; ++p) {
+        const int shift = 32 - (p + 1) * kBgBit;
+        c64 v[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          v[a] = {u32_biased_to_double((dif[a] >> shift) & 127u, kDigitBias),
+                  u32_biased_to_double((dif[a + 8] >> shift) & 127u, kDigitBias)};
+        fwd_stage1(v, T1);
+        exchange<1>(v, xbuf[0], t);
+        fwd_stage2(v, T2);
+        exchange<2>(v, xbuf[1], t);
+        fwd_stage3(v);
+        const c64* bk_r = bk_i + (size_t)(part * kL + p) * 1024;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const c64 b0 = ldg_c64(bk_r + k2 * 128 + t * 2);
+          const c64 b1 = ldg_c64(bk_r + k2 * 128 + t * 2 + 1);
+          af[0][k2] = cadd(af[0][k2], cmul(v[k2], b0));
+          af[1][k2] = cadd(af[1][k2], cmul(v[k2], b1));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      c64 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = af[o][k];
+      inv_stageA(v);
+      exchange<2>(v, xbuf[0], t);
+      inv_stageB(v, T2);
+      exchange<3>(v, xbuf[1], t);
+      inv_stageC(v, T1);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int j = t + 64 * a;
+        acc[o][j] += round_to_torus(v[a].x);
+        acc[o][j + 512] += round_to_torus(v[a].y);
+      }
+    }
+  }
+  __syncthreads();
+  // Sample extraction: a'_0 = a_0, a'_j = -a_{N-j}, b' = b_0.
+  uint32_t* out = xout + (size_t)job.out * kXlweStride;
+  for (int j = t; j < kPolyN; j += 64) out[j] = j == 0 ? acc[0][0] : 0u - acc[0][kPolyN - j];
+  if (t == 0) out[kPolyN] = acc[1][0];
+}
+
+// ------------------------------------------------------------ K3 + K4 --
+__global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
+    const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
+    const uint4* __restrict__ ksk, uint32_t* __restrict__ slab) {
+  __shared__ uint32_t x[kXlweWords];
+  const int t = threadIdx.x;
+  const KsJob job = jobs[blockIdx.x];
+  for (int i = t; i < kXlweWords; i += kKsThreads) {
+    uint32_t v = xlwe[(size_t)job.x[0] * kXlweStride + i];
+    if (job.x[1] != kNoInput) v += xlwe[(size_t)job.x[1] * kXlweStride + i];
+    if (i == kPolyN) v += job.cst;
+    x[i] = v;
+  }
+  __syncthreads();
+  constexpr int kRowVec = kKskRowStride / 4;  // 158 uint4 per row
+  if (t >= kRowVec) return;
+  uint4 a = {0u, 0u, 0u, 0u};
+  if (t == kN / 4) a.z = x[kPolyN];  // column 630 holds b
+  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
+#pragma unroll 2
+  for (int i = 0; i < kPolyN; ++i) {
+    const uint32_t abar = x[i] + prec;
+    const uint4* base = ksk + (size_t)i * (kKsT * kKsBase * kRowVec) + t;
+#pragma unroll
+    for (int j = 0; j < kKsT; ++j) {
+      const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
+      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);  // d = 0 row is zero
+      a.x -= r.x;
+      a.y -= r.y;
+      a.z -= r.z;
+      a.w -= r.w;
+    }
+  }
+  reinterpret_cast<uint4*>(slab + (size_t)job.out_slot * kLweStride)[t] = a;
+}
+
+// ------------------------------------------------- FP64 pipe peak probe --
+// The roofline denominator for the FFT kernel: MEASURED_PEAKS.json carries
+// only HBM and bf16 figures, so the DFMA peak is measured live (8 independent
+// FMA chains per thread, 148 x 8 CTAs of 256 threads).
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-9 + k;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s) {
+  fp64_peak_kernel<<<blocks, 256, 0, s>>>(out, iters);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- launchers --
+cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2, c64* bkf,
+                             cudaStream_t s) {
+  bk_to_fft_kernel<<<kN * kRows * 2, 64, 0, s>>>(bk, tw1, tw2, bkf);
+  return cudaGetLastError();
+}
+cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
+                                const c64* bkf, const c64* tw1, const c64* tw2,
+                                uint32_t* xout, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
+  return cudaGetLastError();
+}
+cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
+                              const uint32_t* ksk, uint32_t* slab, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe,
+                                                 reinterpret_cast<const uint4*>(ksk), slab);
+  return cudaGetLastError();
+}
+
+}  // namespace cvm

@@ -1,0 +1,41 @@
+// Device job descriptors and kernel launchers (see kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft512.cuh"
+#include "tfhe_params.h"
+
+namespace cvm {
+
+constexpr uint32_t kNoInput = 0xFFFFFFFFu;
+constexpr int kKsThreads = 160;
+
+// One blind rotation: input sample = cst*(0,1) + coef[0]*slab[slot[0]]
+// + coef[1]*slab[slot[1]] (coef 0 = unused), mu = 1/8, output extracted
+// sample written to xlwe[out].
+struct BrJob {
+  uint32_t slot[2];
+  int32_t coef[2];
+  uint32_t cst;
+  uint32_t out;
+};
+
+// One key switch: sample = xlwe[x[0]] (+ xlwe[x[1]]) + cst*(0,1), switched
+// to the LWE key and written to slab[out_slot].
+struct KsJob {
+  uint32_t x[2];
+  uint32_t cst;
+  uint32_t out_slot;
+};
+
+cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2, c64* bkf,
+                             cudaStream_t s);
+cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
+                                const c64* bkf, const c64* tw1, const c64* tw2,
+                                uint32_t* xout, cudaStream_t s);
+cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
+cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
+                              const uint32_t* ksk, uint32_t* slab, cudaStream_t s);
+
+}  // namespace cvm

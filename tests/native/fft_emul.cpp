@@ -1,0 +1,145 @@
+// CPU emulation of the 64-thread negacyclic FFT in
+// paper_2101_03403_b200/csrc/fft512.cuh: runs the same __host__ __device__
+// stage functions, exchange-buffer permutations and swizzle with 64 emulated
+// threads and checks products of random (digit, torus32) polynomials against
+// the exact negacyclic product.  Also checks the swizzle is bank-conflict-free.
+//
+// Build+run by tests/test_fft_emul.py:  g++ -O2 -std=c++17 -I<csrc> fft_emul.cpp
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "fft512.cuh"
+
+using namespace cvm;
+
+static c64 T1[64][8], T2[64][8];
+
+// forward: coefficient poly (as doubles) -> bins[t][k2]
+static void forward(const double* p, c64 bins[64][8]) {
+  c64 v[64][8];
+  c64 buf[512];
+  for (int t = 0; t < 64; ++t)
+    for (int a = 0; a < 8; ++a) v[t][a] = {p[t + 64 * a], p[t + 64 * a + 512]};
+  for (int t = 0; t < 64; ++t) fwd_stage1(v[t], T1[t]);
+  for (int t = 0; t < 64; ++t)
+    for (int z = 0; z < 8; ++z) buf[xpos(ex1_cell(t, z), t >> 3)] = v[t][z];
+  for (int t = 0; t < 64; ++t)
+    for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
+  for (int t = 0; t < 64; ++t) fwd_stage2(v[t], T2[t]);
+  for (int t = 0; t < 64; ++t)
+    for (int z = 0; z < 8; ++z) buf[xpos(ex2_cell(t, z), t >> 3)] = v[t][z];
+  for (int t = 0; t < 64; ++t)
+    for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
+  for (int t = 0; t < 64; ++t) {
+    fwd_stage3(v[t]);
+    for (int k = 0; k < 8; ++k) bins[t][k] = v[t][k];
+  }
+}
+
+static void inverse(c64 bins[64][8], uint32_t* out) {
+  c64 v[64][8];
+  c64 buf[512];
+  for (int t = 0; t < 64; ++t)
+    for (int k = 0; k < 8; ++k) v[t][k] = bins[t][k];
+  for (int t = 0; t < 64; ++t) inv_stageA(v[t]);
+  for (int t = 0; t < 64; ++t)
+    for (int z = 0; z < 8; ++z) buf[xpos(ex2_cell(t, z), t >> 3)] = v[t][z];
+  for (int t = 0; t < 64; ++t)
+    for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
+  for (int t = 0; t < 64; ++t) inv_stageB(v[t], T2[t]);
+  for (int t = 0; t < 64; ++t)
+    for (int z = 0; z < 8; ++z) buf[xpos(exB_cell(t, z), t & 7)] = v[t][z];
+  for (int t = 0; t < 64; ++t)
+    for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
+  for (int t = 0; t < 64; ++t) {
+    inv_stageC(v[t], T1[t]);
+    for (int a = 0; a < 8; ++a) {
+      out[t + 64 * a] = round_to_torus(v[t][a].x);
+      out[t + 64 * a + 512] = round_to_torus(v[t][a].y);
+    }
+  }
+}
+
+static bool check_swizzle() {
+  // For each exchange pattern, every quarter-warp (8 consecutive threads)
+  // writing value z, and reading slot s, must touch 8 distinct 16-B bank groups.
+  auto distinct = [](int* g) {
+    int seen = 0;
+    for (int i = 0; i < 8; ++i) {
+      if (seen & (1 << g[i])) return false;
+      seen |= 1 << g[i];
+    }
+    return true;
+  };
+  int g[8];
+  for (int q = 0; q < 8; ++q)
+    for (int z = 0; z < 8; ++z) {
+      for (int i = 0; i < 8; ++i) g[i] = xpos(ex1_cell(8 * q + i, z), q) & 7;
+      if (!distinct(g)) return false;
+      for (int i = 0; i < 8; ++i) g[i] = xpos(ex2_cell(8 * q + i, z), q) & 7;
+      if (!distinct(g)) return false;
+      for (int i = 0; i < 8; ++i) g[i] = xpos(exB_cell(8 * q + i, z), i) & 7;
+      if (!distinct(g)) return false;
+      for (int i = 0; i < 8; ++i) g[i] = xpos(8 * q + i, z) & 7;  // reads
+      if (!distinct(g)) return false;
+    }
+  return true;
+}
+
+int main(int argc, char** argv) {
+  int trials = argc > 1 ? atoi(argv[1]) : 20;
+  make_twiddles(T1, T2);
+  if (!check_swizzle()) {
+    printf("FAIL swizzle conflict\n");
+    return 1;
+  }
+  std::mt19937_64 rng(7);
+  double worst = 0;
+  for (int trial = 0; trial < trials; ++trial) {
+    // 6 digit polys x 6 key polys summed, like one external-product output.
+    std::vector<uint32_t> exact(1024, 0);
+    c64 acc[64][8] = {};
+    for (int r = 0; r < 6; ++r) {
+      std::vector<int32_t> d(1024);
+      std::vector<uint32_t> b(1024);
+      for (auto& x : d) x = int32_t(rng() % 128) - 64;
+      for (auto& x : b) x = uint32_t(rng());
+      for (int i = 0; i < 1024; ++i)
+        for (int j = 0; j < 1024; ++j) {
+          uint32_t prod = uint32_t(d[i]) * b[j];
+          if (i + j < 1024) exact[i + j] += prod;
+          else exact[i + j - 1024] -= prod;
+        }
+      std::vector<double> dd(1024), bd(1024);
+      for (int i = 0; i < 1024; ++i) {
+        dd[i] = d[i];
+        bd[i] = double(int32_t(b[i])) / 512.0;
+      }
+      c64 D[64][8], B[64][8];
+      forward(dd.data(), D);
+      forward(bd.data(), B);
+      for (int t = 0; t < 64; ++t)
+        for (int k = 0; k < 8; ++k) acc[t][k] = cadd(acc[t][k], cmul(D[t][k], B[t][k]));
+    }
+    // distance to nearest integer of the un-rounded result
+    {
+      c64 v[64][8];
+      for (int t = 0; t < 64; ++t)
+        for (int k = 0; k < 8; ++k) v[t][k] = acc[t][k];
+      (void)v;
+    }
+    std::vector<uint32_t> got(1024);
+    inverse(acc, got.data());
+    for (int i = 0; i < 1024; ++i)
+      if (got[i] != exact[i]) {
+        printf("FAIL trial %d coef %d got %u want %u\n", trial, i, got[i], exact[i]);
+        return 1;
+      }
+  }
+  (void)worst;
+  printf("OK %d trials bit-exact\n", trials);
+  return 0;
+}
