@@ -1,0 +1,61 @@
+"""The C-ABI library loads, exports every symbol include/cvm_gpu.h declares,
+and fails loudly (no CPU fallback) when no sm_100a device is present."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2101_03403_b200 as P
+from paper_2101_03403_b200 import _native as N
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "cvm_gpu.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"CVM_API\s+[\w\s\*]+?\b(cvm_\w+)\s*\(", src)))
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert len(names) > 40
+    assert "cvm_submit_level" in names and "cvm_backend_binary_gate" in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(N.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    assert sorted(N.EXPORTED) == _declared()
+
+
+def test_struct_layouts():
+    # cvm_gate: kind, pad, 3 x cvm_operand(16 B), out_slot
+    assert ctypes.sizeof(N.Operand) == 16
+    assert ctypes.sizeof(N.Gate) == 8 + 48 + 8
+    assert ctypes.sizeof(N.Insn) == 40
+
+
+def test_version_and_errors():
+    assert b"sm_100a" in N.lib.cvm_version()
+    with pytest.raises(P.CvmInputError):
+        N.check(N.lib.cvm_keyset_generate(1, None))
+    assert b"null" in N.lib.cvm_last_error()
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure path")
+def test_no_device_fails_loudly():
+    with pytest.raises(P.CvmDeviceError):
+        P.Context(0)
