@@ -180,6 +180,22 @@ CVM_API int cvm_backend_pop_region(cvm_backend* b);
 CVM_API int cvm_backend_fence(cvm_backend* b);
 CVM_API int cvm_backend_flush(cvm_backend* b);
 
+/* Plans: the backend's pending (unflushed) levels moved into a reusable object
+ * with device-resident job tables -- a recorded circuit that can be replayed
+ * on new inputs written into the same input slots (cvm_upload_lwe), either as
+ * plain launches or as one CUDA graph.  Pending uploads are enqueued at
+ * capture; results land in the same slots on every run. */
+typedef struct cvm_plan cvm_plan;
+CVM_API int cvm_backend_capture_plan(cvm_backend* b, cvm_plan** out);
+CVM_API int cvm_plan_run(cvm_ctx* ctx, cvm_plan* plan, int use_graph);
+CVM_API int cvm_plan_info(const cvm_plan* plan, uint64_t* levels, uint64_t* gates,
+                          uint64_t* bootstraps);
+CVM_API void cvm_plan_destroy(cvm_plan* plan);
+/* Slot id backing a handle (-1 for a pure constant); sign/constant of its
+ * linear form (NOT/COPY/CONSTANT folding). */
+CVM_API int cvm_backend_handle_slot(const cvm_backend* b, cvm_handle h, int64_t* slot,
+                                    int32_t* sign, uint32_t* constant);
+
 typedef struct cvm_backend_stats {
   uint64_t nodes, bootstrapped, bootstraps, levels_run, flushes, decrypts;
   uint64_t last_flush_levels, last_flush_gates, max_level_width;

@@ -121,7 +121,14 @@ _SIGS = {
     "cvm_backend_stats_get": (_i, [_p, ctypes.POINTER(BackendStats)]),
     "cvm_backend_node_count": (_i, [_p, _u64p]),
     "cvm_backend_nodes": (_i, [_p, _u64, _u64, _p]),
-    "cvm_fu_out_width": (_i, [_u32, _u32]),
+    "cvm_backend_capture_plan": (_i, [_p, ctypes.POINTER(_p)]),
+    "cvm_plan_run": (_i, [_p, _p, _i]),
+    "cvm_plan_info": (_i, [_p, _u64p, _u64p, _u64p]),
+    "cvm_plan_destroy": (None, [_p]),
+    "cvm_backend_handle_slot": (_i, [_p, _u64, ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_uint32)]),
+    "cvm_fu_out_width":(_i, [_u32, _u32]),
     "cvm_fu_apply": (_i, [_p, _u32, _u32, _p, _p, _p, _p]),
     "cvm_fu_batch": (_i, [_p, _u32, _u32, _u64, _p, _p, _p, _p,
                           ctypes.POINTER(BackendStats)]),

@@ -263,6 +263,17 @@ class Backend:
     def flush(self):
         check(lib.cvm_backend_flush(self._h))
 
+    def capture_plan(self):
+        h = ctypes.c_void_p()
+        check(lib.cvm_backend_capture_plan(self._h, ctypes.byref(h)))
+        return Plan(h)
+
+    def handle_slot(self, h):
+        s, sg, c = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_uint32()
+        check(lib.cvm_backend_handle_slot(self._h, h, ctypes.byref(s), ctypes.byref(sg),
+                                          ctypes.byref(c)))
+        return s.value, sg.value, c.value
+
     def stats(self):
         s = N.BackendStats()
         check(lib.cvm_backend_stats_get(self._h, ctypes.byref(s)))
@@ -312,6 +323,28 @@ class Backend:
         check(lib.cvm_machine_run(self._h, word_size, register_count, _vp(mem), len(memory),
                                   arr, len(program), _vp(regs), _vp(nzcv)))
         return regs.reshape(register_count, word_size), nzcv
+
+
+class Plan:
+    """A recorded circuit (levels with device-resident job tables)."""
+
+    def __init__(self, h):
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.cvm_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def run(self, ctx, graph=True):
+        check(lib.cvm_plan_run(ctx.handle, self._h, 1 if graph else 0))
+
+    def info(self):
+        lv, g, b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.cvm_plan_info(self._h, ctypes.byref(lv), ctypes.byref(g), ctypes.byref(b)))
+        return {"levels": lv.value, "gates": g.value, "bootstraps": b.value}
 
 
 def fu_batch(ctx, op, width, a_lwe, b_lwe, c_lwe=None):

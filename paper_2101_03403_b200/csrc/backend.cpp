@@ -216,6 +216,21 @@ void GpuBackend::flush() {
   for (Node& n : nodes_) n.level = 0;  // everything is now resident
 }
 
+// Moves the pending levels into a replayable plan (uploads are enqueued now).
+Plan* GpuBackend::capture_plan() {
+  std::lock_guard<std::mutex> lock(mu_);
+  context_reserve(ctx_, context_slots_used(ctx_));
+  stage_uploads();
+  Plan* p = context_make_plan(ctx_, pending_levels_);
+  for (const auto& lv : pending_levels_)
+    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, lv.size());
+  stats_.last_flush_levels = pending_levels_.size();
+  stats_.last_flush_gates = p->gates;
+  pending_levels_.clear();
+  for (Node& n : nodes_) n.level = 0;  // resident once the plan has run
+  return p;
+}
+
 void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
   for (size_t i = 0; i < count; ++i) node(hs[i], "export");
   flush();

@@ -404,6 +404,44 @@ int cvm_backend_nodes(const cvm_backend* b, uint64_t first, uint64_t count, int6
   });
 }
 
+int cvm_backend_capture_plan(cvm_backend* b, cvm_plan** out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    if (!b->gpu) throw InputError("the cleartext recorder cannot capture device plans");
+    *out = reinterpret_cast<cvm_plan*>(b->gpu->capture_plan());
+  });
+}
+int cvm_plan_run(cvm_ctx* c, cvm_plan* p, int use_graph) {
+  return guard([&] {
+    need(c, "ctx");
+    need(p, "plan");
+    context_run_plan(c->ctx, reinterpret_cast<Plan*>(p), use_graph != 0);
+  });
+}
+int cvm_plan_info(const cvm_plan* p, uint64_t* levels, uint64_t* gates, uint64_t* boots) {
+  return guard([&] {
+    need(p, "plan");
+    const Plan* q = reinterpret_cast<const Plan*>(p);
+    if (levels) *levels = q->levels.size();
+    if (gates) *gates = q->gates;
+    if (boots) *boots = q->bootstraps;
+  });
+}
+void cvm_plan_destroy(cvm_plan* p) { delete reinterpret_cast<Plan*>(p); }
+int cvm_backend_handle_slot(const cvm_backend* b, cvm_handle h, int64_t* slot, int32_t* sign,
+                            uint32_t* constant) {
+  return guard([&] {
+    need(b, "backend");
+    const std::vector<Node>& ns = b->gpu ? b->gpu->nodes() : b->clear->nodes();
+    if (h == 0 || h > ns.size()) throw InputError("invalid bit handle");
+    const Node& n = ns[h - 1];
+    if (slot) *slot = n.slot;
+    if (sign) *sign = n.sign;
+    if (constant) *constant = n.constant;
+  });
+}
+
 // ----------------------------------------------------- functional units --
 int cvm_fu_out_width(uint32_t op, uint32_t width) { return fu_out_width(op, width); }
 

@@ -189,12 +189,9 @@ class Context {
     sync();
   }
 
-  void submit_level(const cvm_gate* gates, uint64_t count) {
-    if (count == 0) return;
-    if (!has_keys_) throw StateError("submit_level before upload_keys");
-    if (!gates) throw InputError("submit_level: null gates");
-    check(cudaSetDevice(device_), "cudaSetDevice");
-    // Expand gates into blind rotations and key switches.
+  // Validates a level and returns its number of blind rotations.
+  uint64_t count_br(const cvm_gate* gates, uint64_t count) const {
+    if (!gates && count) throw InputError("submit_level: null gates");
     uint64_t n_br = 0;
     for (uint64_t g = 0; g < count; ++g) {
       const uint32_t k = gates[g].kind;
@@ -203,9 +200,11 @@ class Context {
       if (gates[g].out_slot >= cap_) throw InputError("submit_level: out_slot beyond capacity");
       n_br += k == uint32_t(GateKind::Mux) ? 2 : 1;
     }
-    if (n_br > xcap_) grow_xlwe(n_br);
-    BrJob* br = static_cast<BrJob*>(host_arena_.alloc(n_br * sizeof(BrJob)));
-    KsJob* ks = static_cast<KsJob*>(host_arena_.alloc(count * sizeof(KsJob)));
+    return n_br;
+  }
+
+  // Expands gates into blind-rotation jobs (MUX: two) and key-switch jobs.
+  void expand(const cvm_gate* gates, uint64_t count, BrJob* br, KsJob* ks) const {
     uint64_t b = 0;
     for (uint64_t g = 0; g < count; ++g) {
       const cvm_gate& gt = gates[g];
@@ -224,24 +223,105 @@ class Context {
         b += 1;
       }
     }
+  }
+
+  void launch_level(const BrJob* d_br, uint64_t n_br, const KsJob* d_ks, uint64_t n_ks) {
+    Prof* p = begin_prof(0);
+    check(launch_blind_rotate(d_br, int(n_br), slab_, bkf_, tw1_, tw2_, xlwe_, stream_),
+          "blind_rotate_kernel");
+    end_prof(p);
+    p = begin_prof(1);
+    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, slab_, stream_),
+          "key_switch_kernel");
+    end_prof(p);
+    stats_.br_launches++;
+    stats_.br_jobs += n_br;
+    stats_.ks_launches++;
+    stats_.ks_jobs += n_ks;
+  }
+
+  void submit_level(const cvm_gate* gates, uint64_t count) {
+    if (count == 0) return;
+    if (!has_keys_) throw StateError("submit_level before upload_keys");
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const uint64_t n_br = count_br(gates, count);
+    if (n_br > xcap_) grow_xlwe(n_br);
+    BrJob* br = static_cast<BrJob*>(host_arena_.alloc(n_br * sizeof(BrJob)));
+    KsJob* ks = static_cast<KsJob*>(host_arena_.alloc(count * sizeof(KsJob)));
+    expand(gates, count, br, ks);
     BrJob* d_br = static_cast<BrJob*>(dev_arena_.alloc(n_br * sizeof(BrJob)));
     KsJob* d_ks = static_cast<KsJob*>(dev_arena_.alloc(count * sizeof(KsJob)));
     check(cudaMemcpyAsync(d_br, br, n_br * sizeof(BrJob), cudaMemcpyHostToDevice, stream_),
           "upload br jobs");
     check(cudaMemcpyAsync(d_ks, ks, count * sizeof(KsJob), cudaMemcpyHostToDevice, stream_),
           "upload ks jobs");
-    Prof* p = begin_prof(0);
-    check(launch_blind_rotate(d_br, int(n_br), slab_, bkf_, tw1_, tw2_, xlwe_, stream_),
-          "blind_rotate_kernel");
-    end_prof(p);
-    p = begin_prof(1);
-    check(launch_key_switch(d_ks, int(count), xlwe_, ksk_, slab_, stream_),
-          "key_switch_kernel");
-    end_prof(p);
-    stats_.br_launches++;
-    stats_.br_jobs += n_br;
-    stats_.ks_launches++;
-    stats_.ks_jobs += count;
+    launch_level(d_br, n_br, d_ks, count);
+  }
+
+  // A captured sequence of levels with device-resident job tables; replayed
+  // as plain launches or as one CUDA graph.
+  Plan* make_plan(const std::vector<std::vector<cvm_gate>>& levels) {
+    if (!has_keys_) throw StateError("plan before upload_keys");
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    auto plan = std::make_unique<Plan>();
+    size_t bytes = 0;
+    std::vector<uint64_t> nbr(levels.size());
+    for (size_t l = 0; l < levels.size(); ++l) {
+      nbr[l] = count_br(levels[l].data(), levels[l].size());
+      bytes += nbr[l] * sizeof(BrJob) + levels[l].size() * sizeof(KsJob) + 512;
+      plan->gates += levels[l].size();
+      plan->bootstraps += nbr[l];
+      plan->max_br = std::max(plan->max_br, nbr[l]);
+    }
+    std::vector<char> host(bytes);
+    check(cudaMalloc(&plan->dmem, bytes ? bytes : 1), "cudaMalloc(plan)");
+    size_t off = 0;
+    for (size_t l = 0; l < levels.size(); ++l) {
+      Plan::Level lv;
+      lv.n_br = nbr[l];
+      lv.n_ks = levels[l].size();
+      const size_t br_off = off, ks_off = (off + nbr[l] * sizeof(BrJob) + 255) & ~size_t(255);
+      off = (ks_off + lv.n_ks * sizeof(KsJob) + 255) & ~size_t(255);
+      expand(levels[l].data(), lv.n_ks, reinterpret_cast<BrJob*>(host.data() + br_off),
+             reinterpret_cast<KsJob*>(host.data() + ks_off));
+      lv.br = reinterpret_cast<BrJob*>(static_cast<char*>(plan->dmem) + br_off);
+      lv.ks = reinterpret_cast<KsJob*>(static_cast<char*>(plan->dmem) + ks_off);
+      plan->levels.push_back(lv);
+    }
+    check(cudaMemcpy(plan->dmem, host.data(), bytes, cudaMemcpyHostToDevice), "upload plan");
+    return plan.release();
+  }
+
+  void run_plan(Plan* p, bool graph) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    if (p->max_br > xcap_) grow_xlwe(p->max_br);
+    if (!graph || profiling) {
+      for (const auto& lv : p->levels) launch_level(lv.br, lv.n_br, lv.ks, lv.n_ks);
+      return;
+    }
+    if (!p->exec || p->graph_slab != slab_ || p->graph_xlwe != xlwe_) {
+      if (p->exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(p->exec));
+      p->exec = nullptr;
+      cudaGraph_t g;
+      check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+      const cvm_kernel_stats saved = stats_;
+      for (const auto& lv : p->levels) launch_level(lv.br, lv.n_br, lv.ks, lv.n_ks);
+      stats_ = saved;
+      check(cudaStreamEndCapture(stream_, &g), "end capture");
+      cudaGraphExec_t ex = nullptr;
+      check(cudaGraphInstantiate(&ex, g, 0), "cudaGraphInstantiate");
+      p->exec = ex;
+      cudaGraphDestroy(g);
+      p->graph_slab = slab_;
+      p->graph_xlwe = xlwe_;
+    }
+    check(cudaGraphLaunch(static_cast<cudaGraphExec_t>(p->exec), stream_), "cudaGraphLaunch");
+    for (const auto& lv : p->levels) {
+      stats_.br_launches++;
+      stats_.br_jobs += lv.n_br;
+      stats_.ks_launches++;
+      stats_.ks_jobs += lv.n_ks;
+    }
   }
 
   void sync() {
@@ -332,13 +412,13 @@ class Context {
   }
 
   void make_br(BrJob& j, uint32_t c, int ca, const cvm_operand& a, int cb,
-               const cvm_operand& bop, uint64_t out) {
+               const cvm_operand& bop, uint64_t out) const {
     j.cst = c + uint32_t(ca) * a.constant + uint32_t(cb) * bop.constant;
     set_term(j, 0, ca, a);
     set_term(j, 1, cb, bop);
     j.out = uint32_t(out);
   }
-  void set_term(BrJob& j, int i, int coef, const cvm_operand& o) {
+  void set_term(BrJob& j, int i, int coef, const cvm_operand& o) const {
     if (o.slot < 0) {
       j.slot[i] = 0;
       j.coef[i] = 0;
@@ -412,6 +492,14 @@ void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe) 
 }
 void context_submit_level(Context* c, const cvm_gate* g, uint64_t n) { c->submit_level(g, n); }
 void context_sync(Context* c) { c->sync(); }
+Plan* context_make_plan(Context* c, const std::vector<std::vector<cvm_gate>>& levels) {
+  return c->make_plan(levels);
+}
+void context_run_plan(Context* c, Plan* p, bool graph) { c->run_plan(p, graph); }
+Plan::~Plan() {
+  if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+  cudaFree(dmem);
+}
 bool context_has_keys(const Context* c) { return c->has_keys(); }
 void context_set_profiling(Context* c, bool on) { c->profiling = on; }
 cvm_kernel_stats context_stats(Context* c) { return c->stats_; }

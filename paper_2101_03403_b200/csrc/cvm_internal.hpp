@@ -37,6 +37,25 @@ struct KeySet {
 
 // ------------------------------------------------------------ device ctx --
 class Context;
+struct BrJob;
+struct KsJob;
+
+// Captured gate levels with device-resident job tables (cvm_plan).
+struct Plan {
+  struct Level {
+    const BrJob* br;
+    uint64_t n_br;
+    const KsJob* ks;
+    uint64_t n_ks;
+  };
+  ~Plan();
+  std::vector<Level> levels;
+  uint64_t gates = 0, bootstraps = 0, max_br = 0;
+  void* dmem = nullptr;
+  void* exec = nullptr;  // cudaGraphExec_t
+  const void* graph_slab = nullptr;
+  const void* graph_xlwe = nullptr;
+};
 Context* context_create(int device);
 void context_destroy(Context* c);
 void context_upload_keys(Context* c, const uint32_t* bk, const uint32_t* ksk);
@@ -48,6 +67,8 @@ void context_upload(Context* c, uint64_t slot, uint64_t count, const uint32_t* l
 void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe);
 void context_submit_level(Context* c, const cvm_gate* gates, uint64_t count);
 void context_sync(Context* c);
+Plan* context_make_plan(Context* c, const std::vector<std::vector<cvm_gate>>& levels);
+void context_run_plan(Context* c, Plan* p, bool graph);
 bool context_has_keys(const Context* c);
 void context_set_profiling(Context* c, bool on);
 cvm_kernel_stats context_stats(Context* c);
@@ -132,6 +153,7 @@ class GpuBackend final : public Backend {
   void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
   void flush();
+  Plan* capture_plan();
   cvm_backend_stats stats() const;
   const std::vector<Node>& nodes() const { return nodes_; }
 
