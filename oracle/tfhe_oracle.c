@@ -348,10 +348,10 @@ void oracle_negacyclic_mul(int mode, const int32_t* digits, const uint32_t* poly
     double a[N], b[N], c[N];
     ff_forward_int(digits, a);
     ff_forward_u32(poly, b);
-    for (int k = 0; k < N / 2; ++k) {
-      double ar = a[2 * k], ai = a[2 * k + 1], br = b[2 * k], bi = b[2 * k + 1];
-      c[2 * k] = ar * br - ai * bi;
-      c[2 * k + 1] = ar * bi + ai * br;
+    for (int k = 0; k < N / 2; ++k) {  /* split spectra: re[0..511], im[512..] */
+      double ar = a[k], ai = a[k + N / 2], br = b[k], bi = b[k + N / 2];
+      c[k] = ar * br - ai * bi;
+      c[k + N / 2] = ar * bi + ai * br;
     }
     ff_inverse_round(c, out);
   }
@@ -365,9 +365,14 @@ uint32_t oracle_modswitch(uint32_t phase) {
 
 /* out = X^a * in, a in [0, 2N) */
 static void mul_xai(uint32_t* out, int a, const uint32_t* in) {
-  for (int j = 0; j < N; ++j) {
-    int m = ((j - a) % (2 * N) + 2 * N) % (2 * N);
-    out[j] = m < N ? in[m] : (uint32_t)(0u - in[m - N]);
+  /* coefficient j takes in[(j - a) mod 2N], negated when that index >= N */
+  if (a < N) {
+    for (int j = 0; j < a; ++j) out[j] = 0u - in[j - a + N];
+    for (int j = a; j < N; ++j) out[j] = in[j - a];
+  } else {
+    const int b = a - N;
+    for (int j = 0; j < b; ++j) out[j] = in[j - b + N];
+    for (int j = b; j < N; ++j) out[j] = 0u - in[j - b];
   }
 }
 
@@ -439,12 +444,15 @@ static void cmux_step(const oracle_keys* k, int i, uint32_t acc[2][N],
       const int row = part * OR_L + p;
       ff_forward_int(dig[part][p], s->ftmp);
       for (int out = 0; out < 2; ++out) {
-        const double* b = k->bk_fft + ((size_t)(i * 6 + row) * 2 + out) * N;
-        double* a = s->ff[out];
+        const double* restrict br = k->bk_fft + ((size_t)(i * 6 + row) * 2 + out) * N;
+        const double* restrict bi = br + N / 2;
+        double* restrict ar = s->ff[out];
+        double* restrict ai = ar + N / 2;
+        const double* restrict xr = s->ftmp;
+        const double* restrict xi = s->ftmp + N / 2;
         for (int q = 0; q < N / 2; ++q) {
-          const double xr = s->ftmp[2 * q], xi = s->ftmp[2 * q + 1];
-          a[2 * q] += xr * b[2 * q] - xi * b[2 * q + 1];
-          a[2 * q + 1] += xr * b[2 * q + 1] + xi * b[2 * q];
+          ar[q] += xr[q] * br[q] - xi[q] * bi[q];
+          ai[q] += xr[q] * bi[q] + xi[q] * br[q];
         }
       }
     }
