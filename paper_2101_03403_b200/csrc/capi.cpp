@@ -228,6 +228,16 @@ int cvm_ctx_sm_count(cvm_ctx* c, int* sms) {
   });
 }
 
+int cvm_set_br_variant(int v) {
+  return guard([&] {
+    if (v == 0) v = cvm::default_br_variant();
+    if (v != 1 && v != 22 && v != 23 && v != 43 && v != 13)
+      throw InputError("unknown blind-rotation kernel variant " + std::to_string(v));
+    cvm::set_br_variant(v);
+  });
+}
+int cvm_get_br_variant(void) { return cvm::br_variant(); }
+
 // -------------------------------------------------------------- backend --
 int cvm_backend_create(cvm_ctx* c, const cvm_keyset* owner, uint64_t enc_seed,
                        cvm_backend** out) {

@@ -249,3 +249,10 @@ void machine_run(Backend& bk, unsigned word_size, unsigned register_count,
                  uint32_t count, std::vector<Word>* regs, alu::Flags* nzcv);
 
 }  // namespace cvm
+
+namespace cvm {
+// Blind-rotation kernel variant selection (kernels.cu).
+int br_variant();
+void set_br_variant(int v);
+int default_br_variant();
+}  // namespace cvm

@@ -185,6 +185,212 @@ __global__ void __launch_bounds__(64) blind_rotate_kernel(
   if (t == 0) out[kPolyN] = acc[1][0];
 }
 
+// ------------------------------------------------- K1 + K2, version 2 --
+// G bootstraps per CTA (64 threads each, independent named barriers), and the
+// bootstrapping key streamed through a ring of S shared-memory stages by the
+// bulk-copy engine (cp.async.bulk -> SASS UBLKCP), one 16 KB TRGSW row
+// (both output polynomials, all 512 bins) per stage, consumed by all G gates.
+// mbarrier "full" (tx-count) / "empty" (64*G arrivals) pairs order the ring.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void group_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int kPattern>
+__device__ __forceinline__ void exchange_g(c64 v[8], c64* buf, int t, int bar_id) {
+#pragma unroll
+  for (int z = 0; z < 8; ++z) {
+    int cell, slot;
+    if (kPattern == 1) {
+      cell = ex1_cell(t, z);
+      slot = t >> 3;
+    } else if (kPattern == 2) {
+      cell = ex2_cell(t, z);
+      slot = t >> 3;
+    } else {
+      cell = exB_cell(t, z);
+      slot = t & 7;
+    }
+    buf[xpos(cell, slot)] = v[z];
+  }
+  group_sync(bar_id);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = buf[xpos(t, s)];
+}
+
+constexpr uint32_t kRowBytes = 1024 * 16;  // one TRGSW row in FFT domain
+
+template <int G, int S>
+struct BrSmem {
+  c64 ring[S][1024];
+  c64 xbuf[G][2][512];
+  uint32_t acc[G][2][kPolyN];
+  uint16_t bar[G][kLweWords + 1];
+  uint64_t full[S], empty[S];
+};
+
+template <int G, int S>
+__global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
+    const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
+    const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
+    uint32_t* __restrict__ xout) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BrSmem<G, S>& sm = *reinterpret_cast<BrSmem<G, S>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int g = tid >> 6, t = tid & 63;
+  const int bar_id = 1 + g;
+  const int jidx = blockIdx.x * G + g;
+  const bool live = jidx < count;
+  const BrJob job = jobs[live ? jidx : 0];
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 64 * G);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  constexpr int kChunks = kN * kRows;
+  if (tid == 0) {
+    for (int q = 0; q < S - 1; ++q) {
+      mbar_expect_tx(&sm.full[q], kRowBytes);
+      bulk_g2s(sm.ring[q], bkf + (size_t)q * 1024, kRowBytes, &sm.full[q]);
+    }
+  }
+
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+  uint32_t* acc0 = sm.acc[g][0];
+  uint32_t* acc1 = sm.acc[g][1];
+  uint16_t* bar = sm.bar[g];
+  for (int i = t; i < kLweWords; i += 64) {
+    uint32_t v = i == kN ? job.cst : 0u;
+    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
+    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
+    bar[i] = (uint16_t)modswitch_2n(v);
+  }
+  group_sync(bar_id);
+  {
+    const int barb = bar[kN];
+    for (int j = t; j < kPolyN; j += 64) {
+      acc0[j] = 0;
+      acc1[j] = (((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu);
+    }
+  }
+
+  int q = 0;  // chunk sequence number = i * 6 + row
+  for (int i = 0; i < kN; ++i) {
+    group_sync(bar_id);
+    const int ai = bar[i];
+    c64 af[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t* accp = part ? acc1 : acc0;
+      uint32_t dif[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int j = t + 64 * (x & 7) + (x >> 3) * 512;
+        const int m = (j - ai) & (2 * kPolyN - 1);
+        const uint32_t r = m < kPolyN ? accp[m] : 0u - accp[m - kPolyN];
+        dif[x] = r - accp[j] + kDecompOffset;
+      }
+#pragma unroll 1
+      for (int p = 0; p < kL; ++p, ++q) {
+        const int shift = 32 - (p + 1) * kBgBit;
+        c64 v[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          v[a] = {u32_biased_to_double((dif[a] >> shift) & 127u, kDigitBias),
+                  u32_biased_to_double((dif[a + 8] >> shift) & 127u, kDigitBias)};
+        fwd_stage1(v, T1);
+        exchange_g<1>(v, sm.xbuf[g][0], t, bar_id);
+        fwd_stage2(v, T2);
+        exchange_g<2>(v, sm.xbuf[g][1], t, bar_id);
+        fwd_stage3(v);
+        // producer: refill the slot chunk q-1 used with chunk q+S-1
+        if (tid == 0 && q + S - 1 < kChunks) {
+          const int nq = q + S - 1, slot = nq % S;
+          if (q >= 1) mbar_wait(&sm.empty[slot], ((q - 1) / S) & 1);
+          mbar_expect_tx(&sm.full[slot], kRowBytes);
+          bulk_g2s(sm.ring[slot], bkf + (size_t)nq * 1024, kRowBytes, &sm.full[slot]);
+        }
+        const int slot = q % S;
+        mbar_wait(&sm.full[slot], (q / S) & 1);
+        const c64* bk_r = sm.ring[slot];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const c64 b0 = bk_r[k2 * 128 + t * 2];
+          const c64 b1 = bk_r[k2 * 128 + t * 2 + 1];
+          af[0][k2] = cadd(af[0][k2], cmul(v[k2], b0));
+          af[1][k2] = cadd(af[1][k2], cmul(v[k2], b1));
+        }
+        mbar_arrive(&sm.empty[slot]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      c64 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = af[o][k];
+      inv_stageA(v);
+      exchange_g<2>(v, sm.xbuf[g][0], t, bar_id);
+      inv_stageB(v, T2);
+      exchange_g<3>(v, sm.xbuf[g][1], t, bar_id);
+      inv_stageC(v, T1);
+      uint32_t* acco = o ? acc1 : acc0;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int j = t + 64 * a;
+        acco[j] += round_to_torus(v[a].x);
+        acco[j + 512] += round_to_torus(v[a].y);
+      }
+    }
+  }
+  group_sync(bar_id);
+  if (!live) return;
+  uint32_t* out = xout + (size_t)job.out * kXlweStride;
+  for (int j = t; j < kPolyN; j += 64) out[j] = j == 0 ? acc0[0] : 0u - acc0[kPolyN - j];
+  if (t == 0) out[kPolyN] = acc1[0];
+}
+
 // ------------------------------------------------------------ K3 + K4 --
 __global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
     const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
@@ -251,12 +457,47 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
   bk_to_fft_kernel<<<kN * kRows * 2, 64, 0, s>>>(bk, tw1, tw2, bkf);
   return cudaGetLastError();
 }
+template <int G, int S>
+static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
+                             const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
+  static bool configured = false;
+  const int smem = int(sizeof(BrSmem<G, S>));
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(blind_rotate_kernel_v2<G, S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  blind_rotate_kernel_v2<G, S><<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf,
+                                                                       tw1, tw2, xout);
+  return cudaGetLastError();
+}
+
+static int g_br_variant = -1;
+int br_variant() {
+  if (g_br_variant < 0) {
+    const char* e = getenv("CVM_BR_KERNEL");
+    g_br_variant = e ? atoi(e) : kDefaultBrVariant;
+  }
+  return g_br_variant;
+}
+void set_br_variant(int v) { g_br_variant = v; }
+int default_br_variant() { return kDefaultBrVariant; }
+
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 uint32_t* xout, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
-  return cudaGetLastError();
+  switch (br_variant()) {
+    case 1:
+      blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
+      return cudaGetLastError();
+    case 22: return launch_v2<2, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 43: return launch_v2<4, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 13: return launch_v2<1, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s) {

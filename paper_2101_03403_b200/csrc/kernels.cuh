@@ -34,6 +34,12 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 uint32_t* xout, cudaStream_t s);
+// Blind-rotation kernel variant: 1 = one bootstrap per 64-thread CTA, key via
+// L1 (__ldg); 10*G + S = G bootstraps per CTA, key streamed through S
+// bulk-copy shared-memory stages.  Env CVM_BR_KERNEL overrides the default.
+constexpr int kDefaultBrVariant = 23;
+int br_variant();
+void set_br_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s);

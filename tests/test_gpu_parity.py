@@ -45,6 +45,34 @@ def test_nand_level_bit_exact(keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), 1 - (a & b))
 
 
+@pytest.mark.parametrize("variant", [1, 13, 22, 23, 43])
+def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
+    """Every blind-rotation kernel variant (one gate per CTA via L1, G gates per
+    CTA on a bulk-copy shared-memory key ring) gives the oracle's ciphertexts,
+    including a partially filled last CTA (n not a multiple of G)."""
+    from paper_2101_03403_b200._native import lib, check
+    n = 13
+    a, b = _bits(n, 3), _bits(n, 4)
+    ca, cb = keyset.encrypt(a, 13), keyset.encrypt(b, 14)
+    old = lib.cvm_get_br_variant()
+    check(lib.cvm_set_br_variant(variant))
+    try:
+        base = ctx.alloc(3 * n)
+        ctx.upload(base, ca)
+        ctx.upload(base + n, cb)
+        ctx.submit_level([("XOR", [(base + i, 1, 0), (base + n + i, -1, 0)],
+                           base + 2 * n + i) for i in range(n)])
+        ctx.sync()
+        out = ctx.download(base + 2 * n, n)
+    finally:
+        check(lib.cvm_set_br_variant(old))
+    # XOR(a, NOT b) with the NOT folded into the operand's sign
+    nb = (np.uint32(0) - cb).astype(np.uint32)
+    ref = oracle_keys.gates(np.full(n, O.XOR, np.uint8), ca, nb)
+    assert np.array_equal(out, ref)
+    assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
+
+
 @pytest.mark.parametrize("kind", list(TRUTH))
 def test_every_binary_gate_truth_table_and_raw(kind, keyset, ctx, oracle_keys):
     a = np.array([0, 0, 1, 1, 0, 1, 1, 0], np.uint8)
