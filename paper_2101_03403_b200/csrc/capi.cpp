@@ -231,7 +231,10 @@ int cvm_ctx_sm_count(cvm_ctx* c, int* sms) {
 int cvm_set_br_variant(int v) {
   return guard([&] {
     if (v == 0) v = cvm::default_br_variant();
-    if (v != 1 && v != 22 && v != 23 && v != 43 && v != 13)
+    static const int known[] = {1, 22, 23, 43, 13, 123, 1233, 143, 1432, 2233, 322, 640, 631};
+    bool ok = false;
+    for (int k : known) ok = ok || k == v;
+    if (!ok)
       throw InputError("unknown blind-rotation kernel variant " + std::to_string(v));
     cvm::set_br_variant(v);
   });

@@ -79,25 +79,31 @@ CVM_HD void dft8(c64 v[8]) {
   c64 o0 = cadd(s2, s3), o2 = csub(s2, s3);
   c64 u = rot(d3);
   c64 o1 = cadd(d2, u), o3 = csub(d2, u);
-  // twiddles W8^k on the odd half
-  c64 w1, w2, w3;
+  // odd half times W8^k; the 1/sqrt(2) scalings fuse into the final +-.
+  // w1 = r*(p1, q1), w3 = r*(p3, q3) with r = 1/sqrt(2).
+  double p1, q1, p3, q3;
+  c64 w2;
   if (!kInverse) {
-    w1 = {(o1.x + o1.y) * kRsqrt2, (o1.y - o1.x) * kRsqrt2};
+    p1 = o1.x + o1.y;
+    q1 = o1.y - o1.x;
     w2 = {o2.y, -o2.x};
-    w3 = {(o3.y - o3.x) * kRsqrt2, -(o3.x + o3.y) * kRsqrt2};
+    p3 = o3.y - o3.x;
+    q3 = -(o3.x + o3.y);
   } else {
-    w1 = {(o1.x - o1.y) * kRsqrt2, (o1.x + o1.y) * kRsqrt2};
+    p1 = o1.x - o1.y;
+    q1 = o1.x + o1.y;
     w2 = {-o2.y, o2.x};
-    w3 = {-(o3.x + o3.y) * kRsqrt2, (o3.x - o3.y) * kRsqrt2};
+    p3 = -(o3.x + o3.y);
+    q3 = o3.x - o3.y;
   }
   v[0] = cadd(e0, o0);
   v[4] = csub(e0, o0);
-  v[1] = cadd(e1, w1);
-  v[5] = csub(e1, w1);
+  v[1] = {fma(kRsqrt2, p1, e1.x), fma(kRsqrt2, q1, e1.y)};
+  v[5] = {fma(-kRsqrt2, p1, e1.x), fma(-kRsqrt2, q1, e1.y)};
   v[2] = cadd(e2, w2);
   v[6] = csub(e2, w2);
-  v[3] = cadd(e3, w3);
-  v[7] = csub(e3, w3);
+  v[3] = {fma(kRsqrt2, p3, e3.x), fma(kRsqrt2, q3, e3.y)};
+  v[7] = {fma(-kRsqrt2, p3, e3.x), fma(-kRsqrt2, q3, e3.y)};
 }
 
 // Physical position (in c64 units) of (cell, slot) in a 512-entry exchange

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(64) bk_to_fft_kernel(const uint32_t* __restric
   const double s = 1.0 / kFftM;
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2)
-    bkf[((size_t)ir * 8 + k2) * 128 + t * 2 + o] = {v[k2].x * s, v[k2].y * s};
+    bkf[((size_t)ir * 8 + k2) * 128 + o * 64 + t] = {v[k2].x * s, v[k2].y * s};
 }
 
 // ------------------------------------------------------------ K1 + K2 --
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(64) blind_rotate_kernel(
         const c64* bk_r = bk_i + (size_t)(part * kL + p) * 1024;
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const c64 b0 = ldg_c64(bk_r + k2 * 128 + t * 2);
-          const c64 b1 = ldg_c64(bk_r + k2 * 128 + t * 2 + 1);
+          const c64 b0 = ldg_c64(bk_r + k2 * 128 + t);
+          const c64 b1 = ldg_c64(bk_r + k2 * 128 + 64 + t);
           af[0][k2] = cadd(af[0][k2], cmul(v[k2], b0));
           af[1][k2] = cadd(af[1][k2], cmul(v[k2], b1));
         }
@@ -255,22 +255,25 @@ __device__ __forceinline__ void exchange_g(c64 v[8], c64* buf, int t, int bar_id
 
 constexpr uint32_t kRowBytes = 1024 * 16;  // one TRGSW row in FFT domain
 
-template <int G, int S>
+template <int G, int S, bool kTwS>
 struct BrSmem {
   c64 ring[S][1024];
   c64 xbuf[G][2][512];
+  c64 tw[kTwS ? 64 : 1][16];  // per-thread T1 (0..7) and T2 (8..15) when kTwS
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
   uint64_t full[S], empty[S];
 };
 
-template <int G, int S>
-__global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
+// kTwS: twiddles read from shared memory instead of 64 registers;
+// kMinB: CTAs per SM the register allocation must allow.
+template <int G, int S, bool kTwS, int kMinB>
+__global__ void __launch_bounds__(64 * G, kMinB) blind_rotate_kernel_v2(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  BrSmem<G, S>& sm = *reinterpret_cast<BrSmem<G, S>*>(smem_raw);
+  BrSmem<G, S, kTwS>& sm = *reinterpret_cast<BrSmem<G, S, kTwS>*>(smem_raw);
   const int tid = threadIdx.x;
   const int g = tid >> 6, t = tid & 63;
   const int bar_id = 1 + g;
@@ -294,8 +297,20 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
     }
   }
 
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
+  c64 T1r[8], T2r[8];
+  const c64* T1 = T1r;
+  const c64* T2 = T2r;
+  if constexpr (kTwS) {
+    for (int e = tid; e < 64 * 8; e += 64 * G) {
+      sm.tw[e >> 3][e & 7] = tw1[e];
+      sm.tw[e >> 3][8 + (e & 7)] = tw2[e];
+    }
+    __syncthreads();
+    T1 = sm.tw[t];
+    T2 = sm.tw[t] + 8;
+  } else {
+    load_twiddles(tw1, tw2, t, T1r, T2r);
+  }
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
   uint16_t* bar = sm.bar[g];
@@ -357,8 +372,8 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
         const c64* bk_r = sm.ring[slot];
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const c64 b0 = bk_r[k2 * 128 + t * 2];
-          const c64 b1 = bk_r[k2 * 128 + t * 2 + 1];
+          const c64 b0 = bk_r[k2 * 128 + t];
+          const c64 b1 = bk_r[k2 * 128 + 64 + t];
           af[0][k2] = cadd(af[0][k2], cmul(v[k2], b0));
           af[1][k2] = cadd(af[1][k2], cmul(v[k2], b1));
         }
@@ -457,19 +472,19 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
   bk_to_fft_kernel<<<kN * kRows * 2, 64, 0, s>>>(bk, tw1, tw2, bkf);
   return cudaGetLastError();
 }
-template <int G, int S>
+template <int G, int S, bool kTwS = false, int kMinB = 1>
 static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
-  const int smem = int(sizeof(BrSmem<G, S>));
+  const int smem = int(sizeof(BrSmem<G, S, kTwS>));
+  auto* kern = blind_rotate_kernel_v2<G, S, kTwS, kMinB>;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(blind_rotate_kernel_v2<G, S>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  blind_rotate_kernel_v2<G, S><<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf,
-                                                                       tw1, tw2, xout);
+  kern<<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
@@ -496,6 +511,16 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 43: return launch_v2<4, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 13: return launch_v2<1, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    // twiddles in shared memory, with / without a higher occupancy target
+    case 123: return launch_v2<2, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 1233: return launch_v2<2, 3, true, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 143: return launch_v2<4, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 1432: return launch_v2<4, 3, true, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 2233: return launch_v2<2, 3, false, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    // 12 warps per SM: 2 CTAs x 3 gates or 1 CTA x 6 gates (170 registers)
+    case 322: return launch_v2<3, 2, false, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 640: return launch_v2<6, 4, false, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 631: return launch_v2<6, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -40,8 +40,9 @@ constexpr size_t kBkWords = size_t(kN) * kRows * 2 * kPolyN;            // u32
 constexpr size_t kKskWords = size_t(kPolyN) * kKsT * kKsBase * kLweWords;  // u32
 
 // Device bootstrapping key in FFT domain: per CMux step i, per TRGSW row,
-// per k2 (0..7), per thread t (0..63), per output poly o (0..1): one complex
-// double = the folded-FFT bin t + 64*k2 of BK[i][row][o], pre-scaled by 1/M.
+// per k2 (0..7), per output poly o (0..1), per thread t (0..63): one complex
+// double = the folded-FFT bin t + 64*k2 of BK[i][row][o], pre-scaled by 1/M
+// (thread-contiguous, so 16-byte loads from the shared ring are conflict-free).
 constexpr size_t kBkfComplexPerStep = size_t(kRows) * 8 * 64 * 2;  // 6144
 constexpr size_t kBkfBytes = size_t(kN) * kBkfComplexPerStep * 16;  // 61,931,520
 
