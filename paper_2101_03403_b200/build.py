@@ -81,6 +81,8 @@ def build_oracle(with_ref=True):
     subprocess.run(["make", "-s", "-C", os.path.join(REPO, "oracle")], check=True)
     if with_ref and os.path.isdir("/root/reference/proj/core/src"):
         subprocess.run(["make", "-s", "-C", os.path.join(REPO, "oracle"), "ref"], check=True)
+        # the cryptovm::Backend shim + demo over the reference's own ALU/emulator
+        subprocess.run(["make", "-s", "-C", os.path.join(REPO, "integration")], check=True)
 
 
 def main():

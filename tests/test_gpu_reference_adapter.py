@@ -1,0 +1,21 @@
+"""The reference's own functional units and emulator (compiled from
+/root/reference/proj/core/src, unmodified) driving the B200 path through the
+cryptovm::Backend shim in integration/ -- the drop-in demonstration.  The demo
+binary is built in the build container (it needs the reference headers) and
+travels to the GPU box with the snapshot."""
+import os
+import subprocess
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(REPO, "integration", "_build", "adapter_demo")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(DEMO), reason="adapter demo not built (needs /root/reference)")
+def test_reference_alu_and_machine_run_on_gpu_backend():
+    r = subprocess.run([DEMO], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ADAPTER OK" in r.stdout
+    assert "mismatches=0" in r.stdout
