@@ -146,6 +146,10 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * variant computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
+/* Key-switch kernel variant: 1 = one gate per CTA; 4/8 = gates per CTA
+ * sharing each digit position's three non-zero KSK rows.  Bit-identical. */
+CVM_API int cvm_set_ks_variant(int variant);
+CVM_API int cvm_get_ks_variant(void);
 
 /* ------------------------------------------------------------------------
  * Backend: the cryptovm::Backend contract (gates.hpp:109-132) over a context.

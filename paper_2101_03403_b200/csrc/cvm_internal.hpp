@@ -255,4 +255,6 @@ namespace cvm {
 int br_variant();
 void set_br_variant(int v);
 int default_br_variant();
+int ks_variant();
+void set_ks_variant(int v);
 }  // namespace cvm

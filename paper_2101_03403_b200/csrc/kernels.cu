@@ -466,6 +466,70 @@ cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s)
   return cudaGetLastError();
 }
 
+// ------------------------------------------------- K3 + K4, multi-gate --
+// GK key switches per CTA.  For every digit position (i, j) the three
+// non-zero KSK rows are loaded once (3 x 16 B per thread) and reused by all
+// GK gates, whose digit selects the row with a warp-uniform branch: L1/L2
+// traffic drops from 0.75*GK rows to 3 rows per position.
+template <int GK>
+__global__ void __launch_bounds__(kKsThreads) key_switch_multi_kernel(
+    const KsJob* __restrict__ jobs, int count, const uint32_t* __restrict__ xlwe,
+    const uint4* __restrict__ ksk, uint32_t* __restrict__ slab) {
+  __shared__ __align__(16) uint32_t xs[kPolyN][GK];  // abar = a_i + 2^15, per gate
+  __shared__ uint32_t bs[GK];
+  const int t = threadIdx.x;
+  const int first = blockIdx.x * GK;
+  const int live = min(GK, count - first);
+  for (int e = t; e < GK * kXlweWords; e += kKsThreads) {
+    const int g = e / kXlweWords, i = e - g * kXlweWords;
+    if (g >= live) continue;
+    const KsJob& job = jobs[first + g];
+    uint32_t v = xlwe[(size_t)job.x[0] * kXlweStride + i];
+    if (job.x[1] != kNoInput) v += xlwe[(size_t)job.x[1] * kXlweStride + i];
+    if (i == kPolyN) bs[g] = v + job.cst;
+    else xs[i][g] = v + (1u << (32 - (1 + kKsBaseBit * kKsT)));
+  }
+  __syncthreads();
+  constexpr int kRowVec = kKskRowStride / 4;
+  if (t >= kRowVec) return;
+  uint4 acc[GK];
+#pragma unroll
+  for (int g = 0; g < GK; ++g) acc[g] = make_uint4(0, 0, 0, 0);
+  if (t == kN / 4) {
+#pragma unroll
+    for (int g = 0; g < GK; ++g) acc[g].z = g < live ? bs[g] : 0u;
+  }
+  for (int i = 0; i < kPolyN; ++i) {
+    uint32_t ab[GK];
+#pragma unroll
+    for (int g = 0; g < GK; ++g) ab[g] = xs[i][g];
+    const uint4* base = ksk + (size_t)i * (kKsT * kKsBase * kRowVec) + t;
+#pragma unroll 2
+    for (int j = 0; j < kKsT; ++j) {
+      const uint4* rows = base + j * kKsBase * kRowVec;
+      const uint4 r1 = __ldg(rows + 1 * kRowVec);
+      const uint4 r2 = __ldg(rows + 2 * kRowVec);
+      const uint4 r3 = __ldg(rows + 3 * kRowVec);
+      const int sh = 32 - (j + 1) * kKsBaseBit;
+#pragma unroll
+      for (int g = 0; g < GK; ++g) {
+        const uint32_t d = (ab[g] >> sh) & 3u;
+        const uint4 r = d == 1 ? r1 : (d == 2 ? r2 : r3);
+        if (d) {
+          acc[g].x -= r.x;
+          acc[g].y -= r.y;
+          acc[g].z -= r.z;
+          acc[g].w -= r.w;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < GK; ++g)
+    if (g < live)
+      reinterpret_cast<uint4*>(slab + (size_t)jobs[first + g].out_slot * kLweStride)[t] = acc[g];
+}
+
 // ----------------------------------------------------------- launchers --
 cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2, c64* bkf,
                              cudaStream_t s) {
@@ -527,9 +591,33 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe,
-                                                 reinterpret_cast<const uint4*>(ksk), slab);
+  const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
+  switch (ks_variant()) {
+    case 1:
+      key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab);
+      break;
+    case 4:
+      key_switch_multi_kernel<4><<<(count + 3) / 4, kKsThreads, 0, s>>>(jobs, count, xlwe, k4,
+                                                                      slab);
+      break;
+    case 8:
+      key_switch_multi_kernel<8><<<(count + 7) / 8, kKsThreads, 0, s>>>(jobs, count, xlwe, k4,
+                                                                      slab);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
+
+static int g_ks_variant = -1;
+int ks_variant() {
+  if (g_ks_variant < 0) {
+    const char* e = getenv("CVM_KS_KERNEL");
+    g_ks_variant = e ? atoi(e) : kDefaultKsVariant;
+  }
+  return g_ks_variant;
+}
+void set_ks_variant(int v) { g_ks_variant = v; }
 
 }  // namespace cvm

@@ -40,6 +40,11 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
 constexpr int kDefaultBrVariant = 23;
 int br_variant();
 void set_br_variant(int v);
+// Key-switch kernel: 1 = one gate per CTA; GK = 4/8/16 gates per CTA sharing
+// the three non-zero KSK rows of every digit position.  Env CVM_KS_KERNEL.
+constexpr int kDefaultKsVariant = 8;
+int ks_variant();
+void set_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s);

@@ -73,6 +73,33 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
+@pytest.mark.parametrize("ks_variant", [1, 4, 8])
+def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
+    """Single- and multi-gate key-switch kernels, with plain gates and MUX
+    (two extracted samples + 1/8) and a partially filled last CTA."""
+    from paper_2101_03403_b200._native import lib, check
+    n = 11
+    s, t, f = _bits(n, 8), _bits(n, 9), _bits(n, 10)
+    cs, ct, cf = keyset.encrypt(s, 61), keyset.encrypt(t, 62), keyset.encrypt(f, 63)
+    old = lib.cvm_get_ks_variant()
+    check(lib.cvm_set_ks_variant(ks_variant))
+    try:
+        base = ctx.alloc(5 * n)
+        for k, c in enumerate((cs, ct, cf)):
+            ctx.upload(base + k * n, c)
+        gates = [("MUX", [(base + i, 1, 0), (base + n + i, 1, 0), (base + 2 * n + i, 1, 0)],
+                  base + 3 * n + i) for i in range(n)]
+        gates += [("ORYN", [(base + i, 1, 0), (base + n + i, 1, 0)], base + 4 * n + i)
+                  for i in range(n)]
+        ctx.submit_level(gates)
+        ctx.sync()
+        mux, oryn = ctx.download(base + 3 * n, n), ctx.download(base + 4 * n, n)
+    finally:
+        check(lib.cvm_set_ks_variant(old))
+    assert np.array_equal(mux, oracle_keys.gates(np.full(n, O.MUX, np.uint8), cs, ct, cf))
+    assert np.array_equal(oryn, oracle_keys.gates(np.full(n, O.ORYN, np.uint8), cs, ct))
+
+
 @pytest.mark.parametrize("kind", list(TRUTH))
 def test_every_binary_gate_truth_table_and_raw(kind, keyset, ctx, oracle_keys):
     a = np.array([0, 0, 1, 1, 0, 1, 1, 0], np.uint8)

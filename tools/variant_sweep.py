@@ -43,6 +43,20 @@ def main():
         res[v] = {"br_ms": best, "bootstraps_per_s": n / (best * 1e-3), "identical": same,
                   "decrypt_ok": ok}
         print(v, res[v], flush=True)
+    check(lib.cvm_set_br_variant(0))
+    for kv in [int(v) for v in os.environ.get("KS_VARIANTS", "1,4,8").split(",")]:
+        check(lib.cvm_set_ks_variant(kv))
+        best = None
+        for _ in range(3):
+            ctx.reset_stats()
+            ctx.flush_l2()
+            ctx.submit_level(gates)
+            ctx.sync()
+            st = ctx.kernel_stats()
+            best = st["ks_ms"] if best is None else min(best, st["ks_ms"])
+        out = ctx.download(base + 2 * n, n)
+        res[f"ks{kv}"] = {"ks_ms": best, "identical": bool(np.array_equal(out, ref))}
+        print(f"ks{kv}", res[f"ks{kv}"], flush=True)
     print(json.dumps(res))
 
 
