@@ -406,6 +406,198 @@ __global__ void __launch_bounds__(64 * G, kMinB) blind_rotate_kernel_v2(
   if (t == 0) out[kPolyN] = acc1[0];
 }
 
+// ------------------------------------------------- K1 + K2, version 3 --
+// As v2, but every thread runs TWO transforms at once: the forward FFTs of
+// the same gadget level of both TRLWE parts (rows p and 3+p), and the two
+// inverse FFTs.  Twice the independent FP64 work between barriers, the same
+// number of barriers.  Exchange buffers are single-buffered (a WAR barrier
+// separates the two exchanges of a transform).  The key ring is consumed in
+// pair order (rows 0,3, 1,4, 2,5 of each step).
+template <int G, int S>
+struct BrSmem3 {
+  c64 ring[S][1024];
+  c64 xbuf[G][2][512];
+  uint32_t acc[G][2][kPolyN];
+  uint16_t bar[G][kLweWords + 1];
+  uint64_t full[S], empty[S];
+};
+
+// chunk q (0 .. 6n-1) -> TRGSW row offset in the FFT-domain key
+__device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
+  const int i = q / 6, k = q - 6 * (q / 6);
+  const int row = (k & 1) * kL + (k >> 1);
+  return bkf + ((size_t)i * kRows + row) * 1024;
+}
+
+template <int kPattern>
+__device__ __forceinline__ void exchange_pair(c64 va[8], c64 vb[8], c64* ba, c64* bb, int t,
+                                              int bar_id) {
+#pragma unroll
+  for (int z = 0; z < 8; ++z) {
+    int cell, slot;
+    if (kPattern == 1) {
+      cell = ex1_cell(t, z);
+      slot = t >> 3;
+    } else if (kPattern == 2) {
+      cell = ex2_cell(t, z);
+      slot = t >> 3;
+    } else {
+      cell = exB_cell(t, z);
+      slot = t & 7;
+    }
+    ba[xpos(cell, slot)] = va[z];
+    bb[xpos(cell, slot)] = vb[z];
+  }
+  group_sync(bar_id);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    va[s] = ba[xpos(t, s)];
+    vb[s] = bb[xpos(t, s)];
+  }
+  group_sync(bar_id);  // WAR: all reads done before the buffers are rewritten
+}
+
+template <int G, int S>
+__global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
+    const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
+    const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
+    uint32_t* __restrict__ xout) {
+  static_assert(S >= 4, "pairs need two chunks in flight plus prefetch");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BrSmem3<G, S>& sm = *reinterpret_cast<BrSmem3<G, S>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int g = tid >> 6, t = tid & 63;
+  const int bar_id = 1 + g;
+  const int jidx = blockIdx.x * G + g;
+  const bool live = jidx < count;
+  const BrJob job = jobs[live ? jidx : 0];
+  constexpr int kChunks = kN * kRows;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 64 * G);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_expect_tx(&sm.full[q], kRowBytes);
+      bulk_g2s(sm.ring[q], chunk_src(bkf, q), kRowBytes, &sm.full[q]);
+    }
+  }
+
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+  uint32_t* acc0 = sm.acc[g][0];
+  uint32_t* acc1 = sm.acc[g][1];
+  uint16_t* bar = sm.bar[g];
+  c64* xa = sm.xbuf[g][0];
+  c64* xb = sm.xbuf[g][1];
+  for (int i = t; i < kLweWords; i += 64) {
+    uint32_t v = i == kN ? job.cst : 0u;
+    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
+    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
+    bar[i] = (uint16_t)modswitch_2n(v);
+  }
+  group_sync(bar_id);
+  {
+    const int barb = bar[kN];
+    for (int j = t; j < kPolyN; j += 64) {
+      acc0[j] = 0;
+      acc1[j] = (((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu);
+    }
+  }
+
+  int q = 0;  // chunk sequence number (pair order)
+  for (int i = 0; i < kN; ++i) {
+    group_sync(bar_id);
+    const int ai = bar[i];
+    c64 af[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
+#pragma unroll 1
+    for (int p = 0; p < kL; ++p, q += 2) {
+      const int shift = 32 - (p + 1) * kBgBit;
+      c64 va[8], vb[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        // digits of (X^ai - 1) * ACC at coefficients j and j + 512, both parts
+        const int j = t + 64 * x;
+        const int m0 = (j - ai) & (2 * kPolyN - 1);
+        const int m1 = (j + 512 - ai) & (2 * kPolyN - 1);
+        const uint32_t ra0 = m0 < kPolyN ? acc0[m0] : 0u - acc0[m0 - kPolyN];
+        const uint32_t ra1 = m1 < kPolyN ? acc0[m1] : 0u - acc0[m1 - kPolyN];
+        const uint32_t rb0 = m0 < kPolyN ? acc1[m0] : 0u - acc1[m0 - kPolyN];
+        const uint32_t rb1 = m1 < kPolyN ? acc1[m1] : 0u - acc1[m1 - kPolyN];
+        const uint32_t da0 = ra0 - acc0[j] + kDecompOffset;
+        const uint32_t da1 = ra1 - acc0[j + 512] + kDecompOffset;
+        const uint32_t db0 = rb0 - acc1[j] + kDecompOffset;
+        const uint32_t db1 = rb1 - acc1[j + 512] + kDecompOffset;
+        va[x] = {u32_biased_to_double((da0 >> shift) & 127u, kDigitBias),
+                 u32_biased_to_double((da1 >> shift) & 127u, kDigitBias)};
+        vb[x] = {u32_biased_to_double((db0 >> shift) & 127u, kDigitBias),
+                 u32_biased_to_double((db1 >> shift) & 127u, kDigitBias)};
+      }
+      fwd_stage1(va, T1);
+      fwd_stage1(vb, T1);
+      exchange_pair<1>(va, vb, xa, xb, t, bar_id);
+      fwd_stage2(va, T2);
+      fwd_stage2(vb, T2);
+      exchange_pair<2>(va, vb, xa, xb, t, bar_id);
+      fwd_stage3(va);
+      fwd_stage3(vb);
+      // producer: refill the slots of chunks q-2, q-1 with chunks q+S-2, q+S-1
+      if (tid == 0) {
+#pragma unroll
+        for (int c = q - 2; c < q; ++c) {
+          if (c < 0 || c + S >= kChunks) continue;
+          const int slot = c % S;
+          mbar_wait(&sm.empty[slot], (c / S) & 1);
+          mbar_expect_tx(&sm.full[slot], kRowBytes);
+          bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+        }
+      }
+      const int sa = q % S, sb = (q + 1) % S;
+      mbar_wait(&sm.full[sa], (q / S) & 1);
+      mbar_wait(&sm.full[sb], ((q + 1) / S) & 1);
+      const c64* bka = sm.ring[sa];
+      const c64* bkb = sm.ring[sb];
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
+        const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
+        af[0][k2] = cadd(cadd(af[0][k2], cmul(va[k2], a0)), cmul(vb[k2], b0));
+        af[1][k2] = cadd(cadd(af[1][k2], cmul(va[k2], a1)), cmul(vb[k2], b1));
+      }
+      mbar_arrive(&sm.empty[sa]);
+      mbar_arrive(&sm.empty[sb]);
+    }
+    inv_stageA(af[0]);
+    inv_stageA(af[1]);
+    exchange_pair<2>(af[0], af[1], xa, xb, t, bar_id);
+    inv_stageB(af[0], T2);
+    inv_stageB(af[1], T2);
+    exchange_pair<3>(af[0], af[1], xa, xb, t, bar_id);
+    inv_stageC(af[0], T1);
+    inv_stageC(af[1], T1);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int j = t + 64 * a;
+      acc0[j] += round_to_torus(af[0][a].x);
+      acc0[j + 512] += round_to_torus(af[0][a].y);
+      acc1[j] += round_to_torus(af[1][a].x);
+      acc1[j + 512] += round_to_torus(af[1][a].y);
+    }
+  }
+  group_sync(bar_id);
+  if (!live) return;
+  uint32_t* out = xout + (size_t)job.out * kXlweStride;
+  for (int j = t; j < kPolyN; j += 64) out[j] = j == 0 ? acc0[0] : 0u - acc0[kPolyN - j];
+  if (t == 0) out[kPolyN] = acc1[0];
+}
+
 // ------------------------------------------------------------ K3 + K4 --
 __global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
     const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
@@ -552,6 +744,22 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
+template <int G, int S>
+static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
+                             const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
+  static bool configured = false;
+  const int smem = int(sizeof(BrSmem3<G, S>));
+  auto* kern = blind_rotate_kernel_v3<G, S>;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf, tw1, tw2, xout);
+  return cudaGetLastError();
+}
+
 static int g_br_variant = -1;
 int br_variant() {
   if (g_br_variant < 0) {
@@ -584,7 +792,10 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     // 12 warps per SM: 2 CTAs x 3 gates or 1 CTA x 6 gates (170 registers)
     case 322: return launch_v2<3, 2, false, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 640: return launch_v2<6, 4, false, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 631: return launch_v2<6, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    // v3: paired transforms per thread
+    case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3045: return launch_v3<4, 5>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3024: return launch_v3<2, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
