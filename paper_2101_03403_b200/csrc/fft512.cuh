@@ -113,16 +113,26 @@ CVM_HD int xpos(int cell, int slot) {
   return cell * 8 + ((slot ^ cell ^ (cell >> 3)) & 7);
 }
 
+// Twiddles held in shared memory as tw[k][thread] (thread-contiguous, so a
+// warp's 16-byte loads are bank-conflict-free); indexable like an array.
+struct StridedTw {
+  const c64* p;  // &tw[0][t]
+  CVM_HD c64 operator[](int k) const { return p[k * 64]; }
+};
+
 // ---------------------------------------------------------------- forward --
 // Input: v[a] = p_{t+64a} + i p_{t+64a+512} (untwisted).
-CVM_HD void fwd_stage1(c64 v[8], const c64 T1[8]) {
+// TW: c64[8] (registers) or StridedTw (shared memory).
+template <class TW>
+CVM_HD void fwd_stage1(c64 v[8], const TW& T1) {
 #pragma unroll
   for (int a = 1; a < 8; ++a) v[a] = cmul(v[a], twist_const(a));
   dft8<false>(v);
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = cmul(v[k], T1[k]);
 }
-CVM_HD void fwd_stage2(c64 v[8], const c64 T2[8]) {
+template <class TW>
+CVM_HD void fwd_stage2(c64 v[8], const TW& T2) {
   dft8<false>(v);
 #pragma unroll
   for (int k = 1; k < 8; ++k) v[k] = cmul(v[k], T2[k]);
@@ -136,13 +146,15 @@ CVM_HD int exB_cell(int t, int z) { return 8 * z + (t >> 3); }  // slot = t & 7
 
 // ---------------------------------------------------------------- inverse --
 CVM_HD void inv_stageA(c64 v[8]) { dft8<true>(v); }
-CVM_HD void inv_stageB(c64 v[8], const c64 T2[8]) {
+template <class TW>
+CVM_HD void inv_stageB(c64 v[8], const TW& T2) {
 #pragma unroll
   for (int k = 1; k < 8; ++k) v[k] = cmul_conj(v[k], T2[k]);
   dft8<true>(v);
 }
 // Output: v[a] = M * (p_{t+64a} + i p_{t+64a+512}) (scale folded into the key).
-CVM_HD void inv_stageC(c64 v[8], const c64 T1[8]) {
+template <class TW>
+CVM_HD void inv_stageC(c64 v[8], const TW& T1) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = cmul_conj(v[k], T1[k]);
   dft8<true>(v);

@@ -13,6 +13,8 @@
 // DESIGN.md section 4 for the roofline of each kernel.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fft512.cuh"
 #include "kernels.cuh"
 
@@ -259,7 +261,7 @@ template <int G, int S, bool kTwS>
 struct BrSmem {
   c64 ring[S][1024];
   c64 xbuf[G][2][512];
-  c64 tw[kTwS ? 64 : 1][16];  // per-thread T1 (0..7) and T2 (8..15) when kTwS
+  c64 tw[kTwS ? 16 : 1][64];  // tw[k][t]: T1 (k 0..7), T2 (k 8..15) when kTwS
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
   uint64_t full[S], empty[S];
@@ -297,19 +299,22 @@ __global__ void __launch_bounds__(64 * G, kMinB) blind_rotate_kernel_v2(
     }
   }
 
+  using TwT = std::conditional_t<kTwS, StridedTw, const c64*>;
   c64 T1r[8], T2r[8];
-  const c64* T1 = T1r;
-  const c64* T2 = T2r;
+  TwT T1, T2;
   if constexpr (kTwS) {
     for (int e = tid; e < 64 * 8; e += 64 * G) {
-      sm.tw[e >> 3][e & 7] = tw1[e];
-      sm.tw[e >> 3][8 + (e & 7)] = tw2[e];
+      const int tt = e >> 3, k = e & 7;
+      sm.tw[k][tt] = tw1[e];
+      sm.tw[8 + k][tt] = tw2[e];
     }
     __syncthreads();
-    T1 = sm.tw[t];
-    T2 = sm.tw[t] + 8;
+    T1 = StridedTw{&sm.tw[0][t]};
+    T2 = StridedTw{&sm.tw[8][t]};
   } else {
     load_twiddles(tw1, tw2, t, T1r, T2r);
+    T1 = T1r;
+    T2 = T2r;
   }
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
@@ -792,6 +797,9 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     // 12 warps per SM: 2 CTAs x 3 gates or 1 CTA x 6 gates (170 registers)
     case 322: return launch_v2<3, 2, false, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 640: return launch_v2<6, 4, false, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 631: return launch_v2<6, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 531: return launch_v2<5, 3, true, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 530: return launch_v2<5, 3, false, 1>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     // v3: paired transforms per thread
     case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3045: return launch_v3<4, 5>(jobs, count, slab, bkf, tw1, tw2, xout, s);
