@@ -188,6 +188,85 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------- other configs ---
+def extra_configs(P, ctx, ks):
+    """Configs 1, 3, 4 and 5 (BASELINE.json configs[0,2,3,4]) run once each
+    through the public batched API (host buffers in and out), with the device
+    time of their kernels; reported beside the headline config-2 line."""
+    import json as _json
+    rng = np.random.default_rng(77)
+    out = {}
+
+    def fu(op, batch, seed):
+        av = rng.integers(0, 1 << WIDTH, batch)
+        bv = rng.integers(0, 1 << WIDTH, batch)
+        a = ks.encrypt_words(av, WIDTH, seed)
+        b = ks.encrypt_words(bv, WIDTH, seed + 1)
+        ctx.reset_stats()
+        t = time.perf_counter()
+        res, st = P.fu_batch(ctx, op, WIDTH, a, b)
+        wall = time.perf_counter() - t
+        k = ctx.kernel_stats()
+        dev_ms = k["br_ms"] + k["ks_ms"]
+        return av, bv, res, {"batch": batch, "bootstrapped_gates": st["bootstrapped"],
+                             "levels": st["last_flush_levels"], "wall_s": wall,
+                             "device_ms": dev_ms,
+                             "ops_per_s_e2e": batch / wall,
+                             "ops_per_s_device": batch / (dev_ms * 1e-3),
+                             "gates_per_s_device": st["bootstrapped"] / (dev_ms * 1e-3)}
+
+    ctx.set_profiling(True)
+    # config 1: 4096 independent NAND, one level
+    n = 4096
+    a_bits, b_bits = rng.integers(0, 2, n), rng.integers(0, 2, n)
+    base = ctx.alloc(3 * n)
+    ctx.upload(base, ks.encrypt(a_bits, 901))
+    ctx.upload(base + n, ks.encrypt(b_bits, 902))
+    ctx.reset_stats()
+    ctx.submit_level([("NAND", [(base + i, 1, 0), (base + n + i, 1, 0)], base + 2 * n + i)
+                      for i in range(n)])
+    ctx.sync()
+    k = ctx.kernel_stats()
+    ok = np.array_equal(ks.decrypt(ctx.download(base + 2 * n, n)), 1 - (a_bits & b_bits))
+    out["config1_nand4096"] = {"gates_per_s_device": n / ((k["br_ms"] + k["ks_ms"]) * 1e-3),
+                               "device_ms": k["br_ms"] + k["ks_ms"], "correct": bool(ok)}
+    # config 3: SUBS/CMP (sub + NZCV) and LSL by an encrypted amount, 256 each
+    av, bv, res, d = fu("cmp", 256, 910)
+    vals = ks.decrypt_words(res[:, :WIDTH].reshape(-1, 631), WIDTH)
+    d["correct"] = bool(np.array_equal(vals, (av - bv) % (1 << WIDTH)))
+    out["config3_cmp16"] = d
+    av, bv, res, d = fu("lsl", 256, 920)
+    vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
+    d["correct"] = bool(np.array_equal(vals, (av << (bv % WIDTH)) % (1 << WIDTH)))
+    out["config3_lsl16"] = d
+    # config 4: 64 x MUL16 (low 16 bits used by the emulator)
+    av, bv, res, d = fu("umul", 64, 930)
+    vals = ks.decrypt_words(res[:, :WIDTH].reshape(-1, 631), WIDTH)
+    d["correct"] = bool(np.array_equal(vals, (av * bv) % (1 << WIDTH)))
+    out["config4_mul16"] = d
+    # config 5: a seeded 64-instruction program + UDIV on 8 encrypted registers
+    meta = _json.load(open(os.path.join(REPO, "tests", "golden", "programs.json")))[0]
+    bk = P.Backend(ctx, ks)
+    mem = [bk.import_lwe(w) for w in ks.encrypt_words(meta["mem"], WIDTH, 940)]
+    regs, nzcv = bk.machine_run([tuple(i) for i in meta["insns"]], mem)
+    ctx.reset_stats()
+    t = time.perf_counter()
+    bk.flush()
+    wall = time.perf_counter() - t
+    k = ctx.kernel_stats()
+    st = bk.stats()
+    ok = [bk.decrypt_word(r) for r in regs] == meta["regs"] and \
+        list(bk.decrypt_bits(nzcv)) == meta["nzcv"]
+    out["config5_program"] = {"instructions": len(meta["insns"]),
+                              "bootstrapped_gates": st["bootstrapped"],
+                              "dataflow_levels": st["last_flush_levels"],
+                              "latency_s": wall, "device_ms": k["br_ms"] + k["ks_ms"],
+                              "instructions_per_s": len(meta["insns"]) / wall,
+                              "correct": bool(ok)}
+    ctx.set_profiling(False)
+    return out
+
+
 # ------------------------------------------------------------------ ours --
 def run_ours(args):
     import paper_2101_03403_b200 as P
@@ -304,6 +383,7 @@ def run_ours(args):
 
     if rank != 0:
         return 0
+    extras = extra_configs(P, ctx, ks) if (ws == 1 and not args.no_extras) else None
     cpu = cpu_baseline() if (ws == 1 and not args.no_cpu) else None
     traffic = None
     prof = os.path.join(REPO, "profiles", "ncu_blind_rotate.json")
@@ -342,6 +422,9 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "kernels": {"blind_rotate_variant": P.api.lib.cvm_get_br_variant(),
+                    "key_switch_variant": P.api.lib.cvm_get_ks_variant()},
+        "other_configs": extras,
     }
     print(json.dumps(line))
     if dist:
@@ -356,6 +439,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the one-shot configs 1/3/4/5 measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -142,7 +142,9 @@ CVM_API int cvm_ctx_fp64_peak(cvm_ctx* ctx, int reps, double* tflops);
 CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
 /* Blind-rotation kernel variant (process-wide): 1 = one bootstrap per CTA with
  * the key read through L1; 10*G+S = G bootstraps per CTA sharing an S-stage
- * bulk-copy shared-memory key ring (22, 23, 43, 13).  0 = default.  Every
+ * bulk-copy shared-memory key ring (22, 23, 43, 13); 30GS = two transforms in
+ * flight per thread (3044).  0 = auto (default): one bootstrap per CTA for
+ * narrow levels, 3044 for wide ones.  Every
  * variant computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);

@@ -780,7 +780,13 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 uint32_t* xout, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  switch (br_variant()) {
+  int variant = br_variant();
+  if (variant == 0) {
+    // auto: narrow levels spread one bootstrap per CTA over as many SMs as
+    // possible (latency); wide levels use the throughput kernel.
+    variant = count <= 2 * 148 ? 13 : 3044;
+  }
+  switch (variant) {
     case 1:
       blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
       return cudaGetLastError();

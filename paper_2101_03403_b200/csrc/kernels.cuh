@@ -37,7 +37,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
 // Blind-rotation kernel variant: 1 = one bootstrap per 64-thread CTA, key via
 // L1 (__ldg); 10*G + S = G bootstraps per CTA, key streamed through S
 // bulk-copy shared-memory stages.  Env CVM_BR_KERNEL overrides the default.
-constexpr int kDefaultBrVariant = 23;
+constexpr int kDefaultBrVariant = 0;  // 0 = auto by level width
 int br_variant();
 void set_br_variant(int v);
 // Key-switch kernel: 1 = one gate per CTA; GK = 4/8/16 gates per CTA sharing
