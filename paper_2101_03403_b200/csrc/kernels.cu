@@ -603,6 +603,158 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
   if (t == 0) out[kPolyN] = acc1[0];
 }
 
+// ---------------------------------------- K1 + K2, latency ("wide") --
+// One bootstrap per CTA of 384 threads for narrow levels (the emulator's
+// instruction stream averages ~90 gates per dataflow level): the six gadget
+// rows of a CMux step are transformed concurrently, one 64-thread group per
+// row; partial products are reduced through shared memory; groups 0 and 1
+// run the two inverse transforms.  Each group streams its own 16 KB key row
+// for the next step with a bulk copy as soon as it has consumed the current
+// one.  Per-step latency ~ 1 forward + 1 inverse transform instead of 8.
+struct WideSmem {
+  c64 bkbuf[kRows][1024];   // 96 KB: this step's six TRGSW rows
+  c64 xbuf[kRows][512];     // 48 KB: one exchange buffer per group
+  c64 red[kL][2][8][64];    // 48 KB: partial sums [pair][o][k2][t]
+  uint32_t acc[2][kPolyN];
+  uint16_t bar[kLweWords + 1];
+  uint64_t full[kRows];
+};
+
+__global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
+    const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
+    const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
+    uint32_t* __restrict__ xout) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  WideSmem& sm = *reinterpret_cast<WideSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int g = tid >> 6, t = tid & 63;  // group g transforms gadget row g
+  const int bar_id = 1 + g;
+  const int part = g / kL, p = g % kL;
+  const BrJob job = jobs[blockIdx.x];
+
+  if (tid == 0) {
+    for (int r = 0; r < kRows; ++r) mbar_init(&sm.full[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    mbar_expect_tx(&sm.full[g], kRowBytes);
+    bulk_g2s(sm.bkbuf[g], bkf + (size_t)g * 1024, kRowBytes, &sm.full[g]);
+  }
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+  for (int i = tid; i < kLweWords; i += 64 * kRows) {
+    uint32_t v = i == kN ? job.cst : 0u;
+    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
+    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
+    sm.bar[i] = (uint16_t)modswitch_2n(v);
+  }
+  __syncthreads();
+  {
+    const int barb = sm.bar[kN];
+    for (int j = tid; j < kPolyN; j += 64 * kRows) {
+      sm.acc[0][j] = 0;
+      sm.acc[1][j] = (((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu);
+    }
+  }
+  const int shift = 32 - (p + 1) * kBgBit;
+  c64* xb = sm.xbuf[g];
+
+  for (int i = 0; i < kN; ++i) {
+    __syncthreads();  // ACC of the previous step complete
+    const int ai = sm.bar[i];
+    const uint32_t* accp = sm.acc[part];
+    c64 v[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      uint32_t d[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = t + 64 * a + 512 * h;
+        const int m = (j - ai) & (2 * kPolyN - 1);
+        const uint32_t r = m < kPolyN ? accp[m] : 0u - accp[m - kPolyN];
+        d[h] = ((r - accp[j] + kDecompOffset) >> shift) & 127u;
+      }
+      v[a] = {u32_biased_to_double(d[0], kDigitBias), u32_biased_to_double(d[1], kDigitBias)};
+    }
+    fwd_stage1(v, T1);
+    exchange_g<1>(v, xb, t, bar_id);
+    group_sync(bar_id);  // WAR on the single exchange buffer
+    fwd_stage2(v, T2);
+    exchange_g<2>(v, xb, t, bar_id);
+    fwd_stage3(v);
+    // partial products of this row with both output polynomials
+    mbar_wait(&sm.full[g], i & 1);
+    const c64* bk = sm.bkbuf[g];
+    c64 pa[8], pb[8];
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      pa[k2] = cmul(v[k2], bk[k2 * 128 + t]);
+      pb[k2] = cmul(v[k2], bk[k2 * 128 + 64 + t]);
+    }
+    group_sync(bar_id);  // the whole group has read its key row
+    if (t == 0 && i + 1 < kN) {
+      mbar_expect_tx(&sm.full[g], kRowBytes);
+      bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + g) * 1024, kRowBytes, &sm.full[g]);
+    }
+    // two-phase reduction of the six partials into three pair sums
+    if (part == 1) {
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        sm.red[p][0][k2][t] = pa[k2];
+        sm.red[p][1][k2][t] = pb[k2];
+      }
+    }
+    __syncthreads();
+    if (part == 0) {
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        sm.red[p][0][k2][t] = cadd(sm.red[p][0][k2][t], pa[k2]);
+        sm.red[p][1][k2][t] = cadd(sm.red[p][1][k2][t], pb[k2]);
+      }
+    }
+    __syncthreads();
+    if (g < 2) {  // group o = g: inverse transform of output polynomial o
+      const int o = g;
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2)
+        v[k2] = cadd(cadd(sm.red[0][o][k2][t], sm.red[1][o][k2][t]), sm.red[2][o][k2][t]);
+      inv_stageA(v);
+      exchange_g<2>(v, sm.xbuf[g], t, bar_id);
+      inv_stageB(v, T2);
+      exchange_g<3>(v, sm.xbuf[g + 2], t, bar_id);
+      inv_stageC(v, T1);
+      uint32_t* acco = sm.acc[o];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int j = t + 64 * a;
+        acco[j] += round_to_torus(v[a].x);
+        acco[j + 512] += round_to_torus(v[a].y);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* out = xout + (size_t)job.out * kXlweStride;
+  for (int j = tid; j < kPolyN; j += 64 * kRows)
+    out[j] = j == 0 ? sm.acc[0][0] : 0u - sm.acc[0][kPolyN - j];
+  if (tid == 0) out[kPolyN] = sm.acc[1][0];
+}
+
+static cudaError_t launch_wide(const BrJob* jobs, int count, const uint32_t* slab,
+                               const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
+                               cudaStream_t s) {
+  static bool configured = false;
+  const int smem = int(sizeof(WideSmem));
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(blind_rotate_wide_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  blind_rotate_wide_kernel<<<count, 64 * kRows, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ K3 + K4 --
 __global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
     const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
@@ -784,9 +936,10 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   if (variant == 0) {
     // auto: narrow levels spread one bootstrap per CTA over as many SMs as
     // possible (latency); wide levels use the throughput kernel.
-    variant = count <= 2 * 148 ? 13 : 3044;
+    variant = count <= 148 ? 9 : count <= 2 * 148 ? 13 : 3044;
   }
   switch (variant) {
+    case 9: return launch_wide(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 1:
       blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
       return cudaGetLastError();
