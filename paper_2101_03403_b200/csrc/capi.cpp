@@ -242,7 +242,7 @@ int cvm_set_br_variant(int v) {
 int cvm_get_br_variant(void) { return cvm::br_variant(); }
 int cvm_set_ks_variant(int v) {
   return guard([&] {
-    if (v != 1 && v != 4 && v != 8)
+    if (v != 0 && v != 1 && v != 4 && v != 6 && v != 8)
       throw InputError("unknown key-switch kernel variant " + std::to_string(v));
     cvm::set_ks_variant(v);
   });

@@ -815,6 +815,62 @@ cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s)
   return cudaGetLastError();
 }
 
+// --------------------------------------------- K3 + K4, latency ("wide") --
+// One key switch per CTA of 6 x 158 threads: the 1024 input coefficients are
+// split into 6 position groups that gather concurrently, then reduced through
+// shared memory -- ~6x shorter dependent load chain for narrow levels.
+constexpr int kKsWidePG = 6;
+constexpr int kKsWideThreads = kKsWidePG * (kKskRowStride / 4);  // 948
+
+__global__ void __launch_bounds__(kKsWideThreads) key_switch_wide_kernel(
+    const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
+    const uint4* __restrict__ ksk, uint32_t* __restrict__ slab) {
+  constexpr int kRowVec = kKskRowStride / 4;
+  __shared__ uint32_t x[kXlweWords];
+  __shared__ uint4 part[kKsWidePG - 1][kRowVec];
+  const int tid = threadIdx.x;
+  const int col = tid % kRowVec, pg = tid / kRowVec;
+  const KsJob job = jobs[blockIdx.x];
+  for (int i = tid; i < kXlweWords; i += kKsWideThreads) {
+    uint32_t v = xlwe[(size_t)job.x[0] * kXlweStride + i];
+    if (job.x[1] != kNoInput) v += xlwe[(size_t)job.x[1] * kXlweStride + i];
+    if (i == kPolyN) v += job.cst;
+    x[i] = v;
+  }
+  __syncthreads();
+  uint4 a = {0u, 0u, 0u, 0u};
+  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
+  const int i0 = pg * kPolyN / kKsWidePG, i1 = (pg + 1) * kPolyN / kKsWidePG;
+#pragma unroll 2
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t abar = x[i] + prec;
+    const uint4* base = ksk + (size_t)i * (kKsT * kKsBase * kRowVec) + col;
+#pragma unroll
+    for (int j = 0; j < kKsT; ++j) {
+      const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
+      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);
+      a.x -= r.x;
+      a.y -= r.y;
+      a.z -= r.z;
+      a.w -= r.w;
+    }
+  }
+  if (pg > 0) part[pg - 1][col] = a;
+  __syncthreads();
+  if (pg == 0) {
+#pragma unroll
+    for (int k = 0; k < kKsWidePG - 1; ++k) {
+      const uint4 r = part[k][col];
+      a.x += r.x;
+      a.y += r.y;
+      a.z += r.z;
+      a.w += r.w;
+    }
+    if (col == kN / 4) a.z += x[kPolyN];  // column 630 holds b
+    reinterpret_cast<uint4*>(slab + (size_t)job.out_slot * kLweStride)[col] = a;
+  }
+}
+
 // ------------------------------------------------- K3 + K4, multi-gate --
 // GK key switches per CTA.  For every digit position (i, j) the three
 // non-zero KSK rows are loaded once (3 x 16 B per thread) and reused by all
@@ -970,9 +1026,14 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
-  switch (ks_variant()) {
+  int variant = ks_variant();
+  if (variant == 0) variant = count <= 2 * 148 ? 6 : 1;  // auto by level width
+  switch (variant) {
     case 1:
       key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab);
+      break;
+    case 6:
+      key_switch_wide_kernel<<<count, kKsWideThreads, 0, s>>>(jobs, xlwe, k4, slab);
       break;
     case 4:
       key_switch_multi_kernel<4><<<(count + 3) / 4, kKsThreads, 0, s>>>(jobs, count, xlwe, k4,

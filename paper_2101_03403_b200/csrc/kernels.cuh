@@ -42,7 +42,9 @@ int br_variant();
 void set_br_variant(int v);
 // Key-switch kernel: 1 = one gate per CTA; GK = 4/8/16 gates per CTA sharing
 // the three non-zero KSK rows of every digit position.  Env CVM_KS_KERNEL.
-constexpr int kDefaultKsVariant = 1;  // measured fastest (profiles/r01_variant_sweep.txt)
+// 0 = auto: 6 (one gate per 948-thread CTA, 6 position groups) for narrow
+// levels, 1 for wide ones (measured fastest there, profiles/).
+constexpr int kDefaultKsVariant = 0;
 int ks_variant();
 void set_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);

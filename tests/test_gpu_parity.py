@@ -73,7 +73,7 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
-@pytest.mark.parametrize("ks_variant", [1, 4, 8])
+@pytest.mark.parametrize("ks_variant", [1, 4, 6, 8])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
     (two extracted samples + 1/8) and a partially filled last CTA."""
