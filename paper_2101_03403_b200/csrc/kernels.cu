@@ -418,10 +418,11 @@ __global__ void __launch_bounds__(64 * G, kMinB) blind_rotate_kernel_v2(
 // number of barriers.  Exchange buffers are single-buffered (a WAR barrier
 // separates the two exchanges of a transform).  The key ring is consumed in
 // pair order (rows 0,3, 1,4, 2,5 of each step).
-template <int G, int S>
+template <int G, int S, bool kTwS = false>
 struct BrSmem3 {
   c64 ring[S][1024];
   c64 xbuf[G][2][512];
+  c64 tw[kTwS ? 16 : 1][64];  // tw[k][t] when kTwS
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
   uint64_t full[S], empty[S];
@@ -462,14 +463,14 @@ __device__ __forceinline__ void exchange_pair(c64 va[8], c64 vb[8], c64* ba, c64
   group_sync(bar_id);  // WAR: all reads done before the buffers are rewritten
 }
 
-template <int G, int S>
+template <int G, int S, bool kTwS = false>
 __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
   static_assert(S >= 4, "pairs need two chunks in flight plus prefetch");
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  BrSmem3<G, S>& sm = *reinterpret_cast<BrSmem3<G, S>*>(smem_raw);
+  BrSmem3<G, S, kTwS>& sm = *reinterpret_cast<BrSmem3<G, S, kTwS>*>(smem_raw);
   const int tid = threadIdx.x;
   const int g = tid >> 6, t = tid & 63;
   const int bar_id = 1 + g;
@@ -493,8 +494,23 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     }
   }
 
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
+  using TwT = std::conditional_t<kTwS, StridedTw, const c64*>;
+  c64 T1r[8], T2r[8];
+  TwT T1, T2;
+  if constexpr (kTwS) {
+    for (int e = tid; e < 64 * 8; e += 64 * G) {
+      const int tt = e >> 3, k = e & 7;
+      sm.tw[k][tt] = tw1[e];
+      sm.tw[8 + k][tt] = tw2[e];
+    }
+    __syncthreads();
+    T1 = StridedTw{&sm.tw[0][t]};
+    T2 = StridedTw{&sm.tw[8][t]};
+  } else {
+    load_twiddles(tw1, tw2, t, T1r, T2r);
+    T1 = T1r;
+    T2 = T2r;
+  }
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
   uint16_t* bar = sm.bar[g];
@@ -957,12 +973,12 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S>
+template <int G, int S, bool kTwS = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
-  const int smem = int(sizeof(BrSmem3<G, S>));
-  auto* kern = blind_rotate_kernel_v3<G, S>;
+  const int smem = int(sizeof(BrSmem3<G, S, kTwS>));
+  auto* kern = blind_rotate_kernel_v3<G, S, kTwS>;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1019,6 +1035,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3045: return launch_v3<4, 5>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3024: return launch_v3<2, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3144: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
