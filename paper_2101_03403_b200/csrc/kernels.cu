@@ -232,6 +232,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void group_sync(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
+// code = barrier id | (thread count << 8)
+__device__ __forceinline__ void group_sync_code(int code) {
+  asm volatile("bar.sync %0, %1;" ::"r"(code & 255), "r"(code >> 8) : "memory");
+}
 
 template <int kPattern>
 __device__ __forceinline__ void exchange_g(c64 v[8], c64* buf, int t, int bar_id) {
@@ -454,26 +458,32 @@ __device__ __forceinline__ void exchange_pair(c64 va[8], c64 vb[8], c64* ba, c64
     ba[xpos(cell, slot)] = va[z];
     bb[xpos(cell, slot)] = vb[z];
   }
-  group_sync(bar_id);
+  group_sync_code(bar_id);
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     va[s] = ba[xpos(t, s)];
     vb[s] = bb[xpos(t, s)];
   }
-  group_sync(bar_id);  // WAR: all reads done before the buffers are rewritten
+  group_sync_code(bar_id);  // WAR: all reads done before the buffers are rewritten
 }
 
-template <int G, int S, bool kTwS = false>
+// kIL (interleaved): warp w holds threads t = 8w..8w+7 of all four gates
+// (lane = 8*g + t%8), so the key-row loads of a warp hit 8 distinct
+// addresses (broadcast across gates) instead of 32; gates then advance in
+// CTA-wide lockstep (bar.sync 0 over 256 threads).
+template <int G, int S, bool kTwS = false, bool kIL = false>
 __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
   static_assert(S >= 4, "pairs need two chunks in flight plus prefetch");
+  static_assert(!kIL || G == 4, "interleaving maps 4 gates onto a warp");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BrSmem3<G, S, kTwS>& sm = *reinterpret_cast<BrSmem3<G, S, kTwS>*>(smem_raw);
   const int tid = threadIdx.x;
-  const int g = tid >> 6, t = tid & 63;
-  const int bar_id = 1 + g;
+  const int g = kIL ? ((tid & 31) >> 3) : (tid >> 6);
+  const int t = kIL ? (8 * (tid >> 5) + (tid & 7)) : (tid & 63);
+  const int bar_id = kIL ? (64 * G) << 8 : ((1 + g) | (64 << 8));
   const int jidx = blockIdx.x * G + g;
   const bool live = jidx < count;
   const BrJob job = jobs[live ? jidx : 0];
@@ -522,7 +532,7 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
     bar[i] = (uint16_t)modswitch_2n(v);
   }
-  group_sync(bar_id);
+  group_sync_code(bar_id);
   {
     const int barb = bar[kN];
     for (int j = t; j < kPolyN; j += 64) {
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
 
   int q = 0;  // chunk sequence number (pair order)
   for (int i = 0; i < kN; ++i) {
-    group_sync(bar_id);
+    group_sync_code(bar_id);
     const int ai = bar[i];
     c64 af[2][8];
 #pragma unroll
@@ -612,7 +622,7 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
       acc1[j + 512] += round_to_torus(af[1][a].y);
     }
   }
-  group_sync(bar_id);
+  group_sync_code(bar_id);
   if (!live) return;
   uint32_t* out = xout + (size_t)job.out * kXlweStride;
   for (int j = t; j < kPolyN; j += 64) out[j] = j == 0 ? acc0[0] : 0u - acc0[kPolyN - j];
@@ -973,12 +983,12 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTwS = false>
+template <int G, int S, bool kTwS = false, bool kIL = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S, kTwS>));
-  auto* kern = blind_rotate_kernel_v3<G, S, kTwS>;
+  auto* kern = blind_rotate_kernel_v3<G, S, kTwS, kIL>;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1036,6 +1046,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 3045: return launch_v3<4, 5>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3024: return launch_v3<2, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3144: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3244: return launch_v3<4, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3344: return launch_v3<4, 4, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
