@@ -208,9 +208,14 @@ CVM_API void cvm_plan_destroy(cvm_plan* plan);
 CVM_API int cvm_backend_handle_slot(const cvm_backend* b, cvm_handle h, int64_t* slot,
                                     int32_t* sign, uint32_t* constant);
 
+/* bootstrapped/bootstraps count recorded gates (MUX = 1 / 2), like
+ * ScheduleReport.bootstrapped_count (sched.cpp:196-199); executed counts the
+ * gates actually evaluated (decrypt/export evaluate only the cone of the
+ * requested handles, so dead gates are skipped); pending = not yet evaluated. */
 typedef struct cvm_backend_stats {
   uint64_t nodes, bootstrapped, bootstraps, levels_run, flushes, decrypts;
   uint64_t last_flush_levels, last_flush_gates, max_level_width;
+  uint64_t executed, executed_bootstraps, pending;
 } cvm_backend_stats;
 CVM_API int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out);
 /* Node table: kind, input flag, deps (0 = none), constant value per node id. */
@@ -233,7 +238,9 @@ typedef enum cvm_fu_op {
   CVM_FU_UMUL = 12,     /* alu::mul_unsigned      out: 2*width            */
   CVM_FU_SMUL = 13,     /* alu::mul_signed        out: 2*width            */
   CVM_FU_UDIV = 14,     /* alu::div_unsigned (Widened) out: width         */
-  CVM_FU_UDIV_EXACT = 15
+  CVM_FU_UDIV_EXACT = 15,
+  CVM_FU_MUL_LO = 16    /* MUL as the emulator issues it: mul_unsigned, low
+                           half kept (emulator.cpp:271-285)  out: width   */
 } cvm_fu_op;
 CVM_API int cvm_fu_out_width(uint32_t op, uint32_t width);
 CVM_API int cvm_fu_apply(cvm_backend* b, uint32_t op, uint32_t width,

@@ -55,7 +55,8 @@ class KernelStats(ctypes.Structure):
 class BackendStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in
                 ("nodes", "bootstrapped", "bootstraps", "levels_run", "flushes", "decrypts",
-                 "last_flush_levels", "last_flush_gates", "max_level_width")]
+                 "last_flush_levels", "last_flush_gates", "max_level_width", "executed",
+                 "executed_bootstraps", "pending")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

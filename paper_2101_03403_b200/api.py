@@ -15,7 +15,7 @@ GATE_KINDS = ["CONSTANT", "NOT", "COPY", "NAND", "AND", "OR", "XOR", "XNOR", "NO
 KIND = {n: i for i, n in enumerate(GATE_KINDS)}
 
 FU_OPS = ["add", "add_cin", "sub", "addsub", "cmp", "and", "orr", "eor", "orn", "lsl",
-          "lsr", "asr", "umul", "smul", "udiv", "udiv_exact"]
+          "lsr", "asr", "umul", "smul", "udiv", "udiv_exact", "mul_lo"]
 FU = {n: i for i, n in enumerate(FU_OPS)}
 
 OPCODES = ["LOAD", "STORE", "MOV", "ADD", "ADDS", "SUB", "SUBS", "MUL", "MULS", "SMUL",

@@ -362,6 +362,7 @@ int fu_out_width(uint32_t op, uint32_t w) {
     case CVM_FU_ASR:
     case CVM_FU_UDIV:
     case CVM_FU_UDIV_EXACT:
+    case CVM_FU_MUL_LO:
       return int(w);
     default:
       return -1;
@@ -401,6 +402,11 @@ Word fu_apply(Backend& bk, uint32_t op, const Word& a, const Word& b, Bit c) {
     case CVM_FU_SMUL: return mul_signed(bk, a, b);
     case CVM_FU_UDIV: return div_unsigned(bk, a, b, DivAccumulator::Widened);
     case CVM_FU_UDIV_EXACT: return div_unsigned(bk, a, b, DivAccumulator::Exact);
+    case CVM_FU_MUL_LO: {
+      Word p = mul_unsigned(bk, a, b);
+      p.resize(a.size());  // the high half's gates are recorded but dead
+      return p;
+    }
     default: throw InputError("unknown functional-unit op " + std::to_string(op));
   }
 }

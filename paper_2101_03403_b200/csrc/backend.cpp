@@ -1,5 +1,6 @@
 // GpuBackend: the cryptovm::Backend contract (gates.hpp:109-132) over the
-// device context, with lazy recording and dataflow levelisation.
+// device context, with lazy recording, dataflow levelisation and
+// demand-driven evaluation.
 //
 // Reference behaviour kept:
 //  * every gate call returns a handle immediately; handles are dense 1-based
@@ -13,8 +14,14 @@
 //    annotation (dag.hpp:44-48): gates are pure, so evaluation
 //    follows dataflow -- the level of a gate is 1 + the deepest level among
 //    its not-yet-evaluated inputs.
-// Evaluation happens at flush points (decrypt / export / explicit flush):
-// each pending level becomes one cvm_submit_level (two launches).
+// Evaluation happens at flush points.  A decrypt / export evaluates only the
+// cone of influence of the requested handles (everything else stays pending
+// and runs if and when something needs it): gates are pure, so results are
+// unchanged, and circuits whose outputs are partly discarded -- the
+// emulator's MUL keeps the low half of a 2N-bit product (emulator.cpp:271-285),
+// registers get overwritten, CMP flags get replaced -- skip their dead gates
+// (SURVEY.md section 8 f-3).  cvm_backend_flush evaluates everything pending.
+// Each level becomes one cvm_submit_level (two launches).
 #include <algorithm>
 #include <cstring>
 
@@ -34,6 +41,10 @@ int bootstrap_count(GateKind k) {
       return 1;
   }
 }
+
+namespace {
+bool is_gate(GateKind k) { return k >= GateKind::Nand; }
+}  // namespace
 
 GpuBackend::GpuBackend(Context* ctx, const KeySet* owner, uint64_t enc_seed)
     : ctx_(ctx), owner_(owner), enc_seed_(enc_seed) {
@@ -57,6 +68,17 @@ Bit GpuBackend::add_node(Node n) {
 cvm_operand GpuBackend::operand(Bit h) const {
   const Node& n = nodes_[h - 1];
   return cvm_operand{n.slot, n.sign, n.constant};
+}
+
+Bit GpuBackend::record_gate(Node n, const cvm_gate& g) {
+  n.gate_idx = uint32_t(gates_.size());
+  gates_.push_back(g);
+  const Bit id = add_node(n);
+  pending_.push_back(id);
+  first_pending_ = std::min<uint64_t>(first_pending_, id);
+  stats_.bootstrapped++;
+  stats_.bootstraps += uint64_t(bootstrap_count(n.kind));
+  return id;
 }
 
 Bit GpuBackend::constant(bool value) {
@@ -102,18 +124,13 @@ Bit GpuBackend::binary_gate(GateKind kind, Bit a, Bit b) {
   n.level = std::max(na.level, nb.level) + 1;
   n.slot = int64_t(take_slot());
   n.sign = 1;
-  n.constant = 0;
   cvm_gate g{};
   g.kind = uint32_t(kind);
   g.in[0] = operand(a);
   g.in[1] = operand(b);
   g.in[2] = cvm_operand{-1, 1, 0};
   g.out_slot = uint64_t(n.slot);
-  if (pending_levels_.size() < n.level) pending_levels_.resize(n.level);
-  pending_levels_[n.level - 1].push_back(g);
-  stats_.bootstrapped++;
-  stats_.bootstraps++;
-  return add_node(n);
+  return record_gate(n, g);
 }
 
 Bit GpuBackend::mux_gate(Bit sel, Bit on_true, Bit on_false) {
@@ -136,11 +153,7 @@ Bit GpuBackend::mux_gate(Bit sel, Bit on_true, Bit on_false) {
   g.in[1] = operand(on_true);
   g.in[2] = operand(on_false);
   g.out_slot = uint64_t(n.slot);
-  if (pending_levels_.size() < n.level) pending_levels_.resize(n.level);
-  pending_levels_[n.level - 1].push_back(g);
-  stats_.bootstrapped++;
-  stats_.bootstraps += 2;
-  return add_node(n);
+  return record_gate(n, g);
 }
 
 Bit GpuBackend::encrypt_bit(bool value) {
@@ -195,45 +208,121 @@ void GpuBackend::stage_uploads() {
   pending_upload_.clear();
 }
 
-void GpuBackend::flush() {
-  std::lock_guard<std::mutex> lock(mu_);
-  if (pending_upload_.empty() && pending_levels_.empty()) return;
+// Groups the selected pending gates by level (their pending inputs are
+// selected too, so levels stay consistent).
+std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(const std::vector<Bit>& ids) const {
+  std::vector<std::vector<cvm_gate>> lv;
+  for (Bit id : ids) {
+    const Node& n = nodes_[id - 1];
+    if (lv.size() < n.level) lv.resize(n.level);
+    lv[n.level - 1].push_back(gates_[n.gate_idx]);
+  }
+  lv.erase(std::remove_if(lv.begin(), lv.end(), [](const auto& v) { return v.empty(); }),
+           lv.end());
+  return lv;
+}
+
+// After the gates in `done` became resident: recompute the levels of what is
+// still pending (node ids are a topological order) and drop `done`.
+void GpuBackend::retire(const std::vector<Bit>& done) {
+  for (Bit id : done) nodes_[id - 1].level = 0;
+  if (done.size() == pending_.size()) {
+    pending_.clear();
+    for (uint64_t i = first_pending_; i <= nodes_.size(); ++i) nodes_[i - 1].level = 0;
+    first_pending_ = UINT64_MAX;
+    return;
+  }
+  std::vector<Bit> still;
+  still.reserve(pending_.size() - done.size());
+  for (Bit id : pending_)
+    if (nodes_[id - 1].level != 0) still.push_back(id);
+  pending_.swap(still);
+  const uint64_t from = pending_.empty() ? nodes_.size() + 1 : pending_.front();
+  for (uint64_t i = first_pending_; i <= nodes_.size(); ++i) {
+    Node& n = nodes_[i - 1];
+    if (n.level == 0) continue;
+    uint32_t lv = 0;
+    for (int d = 0; d < n.ndeps; ++d) lv = std::max(lv, nodes_[n.dep[d] - 1].level);
+    n.level = is_gate(n.kind) ? lv + 1 : lv;
+  }
+  first_pending_ = from;
+}
+
+void GpuBackend::run(const std::vector<Bit>& ids) {
   context_reserve(ctx_, context_slots_used(ctx_));
   stage_uploads();
-  uint64_t gates = 0;
-  for (const auto& lv : pending_levels_) {
-    context_submit_level(ctx_, lv.data(), lv.size());
-    gates += lv.size();
-    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, lv.size());
+  const auto lv = levels_of(ids);
+  uint64_t gates = 0, boots = 0;
+  for (const auto& level : lv) {
+    context_submit_level(ctx_, level.data(), level.size());
+    gates += level.size();
+    for (const auto& g : level) boots += g.kind == uint32_t(GateKind::Mux) ? 2 : 1;
+    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, level.size());
   }
   context_sync(ctx_);
   stats_.flushes++;
-  stats_.levels_run += pending_levels_.size();
-  stats_.last_flush_levels = pending_levels_.size();
+  stats_.levels_run += lv.size();
+  stats_.last_flush_levels = lv.size();
   stats_.last_flush_gates = gates;
-  pending_upload_.clear();
-  pending_levels_.clear();
-  for (Node& n : nodes_) n.level = 0;  // everything is now resident
+  stats_.executed += gates;
+  stats_.executed_bootstraps += boots;
+  retire(ids);
 }
 
-// Moves the pending levels into a replayable plan (uploads are enqueued now).
+void GpuBackend::flush() {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (pending_.empty()) {
+    stage_uploads();
+    return;
+  }
+  const std::vector<Bit> all = pending_;
+  run(all);
+}
+
+// Evaluates the cone of influence of `hs` only.
+void GpuBackend::flush_for(size_t count, const Bit* hs) {
+  std::lock_guard<std::mutex> lock(mu_);
+  std::vector<Bit> need, stack;
+  std::vector<uint8_t> seen;
+  for (size_t i = 0; i < count; ++i)
+    if (nodes_[hs[i] - 1].level != 0) stack.push_back(hs[i]);
+  if (stack.empty()) {
+    stage_uploads();
+    return;
+  }
+  seen.assign(nodes_.size() - first_pending_ + 1, 0);
+  while (!stack.empty()) {
+    const Bit id = stack.back();
+    stack.pop_back();
+    const Node& n = nodes_[id - 1];
+    if (n.level == 0 || seen[id - first_pending_]) continue;
+    seen[id - first_pending_] = 1;
+    if (is_gate(n.kind)) need.push_back(id);
+    for (int d = 0; d < n.ndeps; ++d) stack.push_back(n.dep[d]);
+  }
+  std::sort(need.begin(), need.end());
+  run(need);
+}
+
+// Moves every pending level into a replayable plan (uploads are enqueued now).
 Plan* GpuBackend::capture_plan() {
   std::lock_guard<std::mutex> lock(mu_);
   context_reserve(ctx_, context_slots_used(ctx_));
   stage_uploads();
-  Plan* p = context_make_plan(ctx_, pending_levels_);
-  for (const auto& lv : pending_levels_)
-    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, lv.size());
-  stats_.last_flush_levels = pending_levels_.size();
+  const std::vector<Bit> all = pending_;
+  const auto lv = levels_of(all);
+  Plan* p = context_make_plan(ctx_, lv);
+  for (const auto& level : lv)
+    stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, level.size());
+  stats_.last_flush_levels = lv.size();
   stats_.last_flush_gates = p->gates;
-  pending_levels_.clear();
-  for (Node& n : nodes_) n.level = 0;  // resident once the plan has run
+  if (!all.empty()) retire(all);  // resident once the plan has run
   return p;
 }
 
 void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
   for (size_t i = 0; i < count; ++i) node(hs[i], "export");
-  flush();
+  flush_for(count, hs);
   std::lock_guard<std::mutex> lock(mu_);
   // Download the covering slot range in runs, then apply the linear forms.
   std::vector<int64_t> slots;
@@ -300,6 +389,10 @@ void GpuBackend::fence() {
   ++fences_;
 }
 
-cvm_backend_stats GpuBackend::stats() const { return stats_; }
+cvm_backend_stats GpuBackend::stats() const {
+  cvm_backend_stats s = stats_;
+  s.pending = pending_.size();
+  return s;
+}
 
 }  // namespace cvm

@@ -129,6 +129,7 @@ struct Node {
   bool const_value;
   uint8_t ndeps;
   uint32_t level;       // dataflow level (bootstrapped depth), 0 = available
+  uint32_t gate_idx;    // GpuBackend: index of the recorded cvm_gate
   Bit dep[3];
   // Linear form of the node's ciphertext: sign * slab[slot] + constant.
   int64_t slot;         // -1: pure constant
@@ -152,7 +153,8 @@ class GpuBackend final : public Backend {
   void decrypt_bits(size_t n, const Bit* hs, uint8_t* out);
   void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
-  void flush();
+  void flush();                             // everything pending
+  void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only
   Plan* capture_plan();
   cvm_backend_stats stats() const;
   const std::vector<Node>& nodes() const { return nodes_; }
@@ -160,9 +162,13 @@ class GpuBackend final : public Backend {
  private:
   const Node& node(Bit h, const char* what) const;
   Bit add_node(Node n);
+  Bit record_gate(Node n, const cvm_gate& g);
   cvm_operand operand(Bit h) const;
   uint64_t take_slot();
   void stage_uploads();
+  std::vector<std::vector<cvm_gate>> levels_of(const std::vector<Bit>& ids) const;
+  void run(const std::vector<Bit>& ids);
+  void retire(const std::vector<Bit>& done);
 
   std::mutex mu_;
   Context* ctx_;
@@ -171,10 +177,12 @@ class GpuBackend final : public Backend {
   uint64_t enc_counter_ = 0;
   std::vector<Node> nodes_;          // nodes_[id - 1]
   uint64_t next_slot_ = 0, chunk_end_ = 0, chunk_ = 4096;  // slot chunk from ctx
-  // pending uploads (fresh encryptions / imports) and gates, by level
+  // pending uploads (fresh encryptions / imports) and recorded gates
   std::vector<uint32_t> pending_upload_;
   uint64_t pending_upload_slot_ = 0;
-  std::vector<std::vector<cvm_gate>> pending_levels_;
+  std::vector<cvm_gate> gates_;     // every recorded gate (node.gate_idx)
+  std::vector<Bit> pending_;        // not yet evaluated gate nodes, id order
+  uint64_t first_pending_ = UINT64_MAX;
   std::vector<std::string> regions_;
   uint64_t fences_ = 0;
   cvm_backend_stats stats_{};
