@@ -191,6 +191,13 @@ CVM_API int cvm_backend_push_region(cvm_backend* b, const char* name);
 CVM_API int cvm_backend_pop_region(cvm_backend* b);
 CVM_API int cvm_backend_fence(cvm_backend* b);
 CVM_API int cvm_backend_flush(cvm_backend* b);
+/* Flush policy of decrypt/export: CVM_FLUSH_CONE (default) evaluates only the
+ * cone of influence of the requested handles -- dead gates are never run;
+ * CVM_FLUSH_ALL evaluates everything pending at the first decrypt, for callers
+ * that decrypt one bit at a time (the reference's decrypt_word, word.cpp:70-77). */
+#define CVM_FLUSH_CONE 0
+#define CVM_FLUSH_ALL 1
+CVM_API int cvm_backend_set_flush_policy(cvm_backend* b, int policy);
 
 /* Plans: the backend's pending (unflushed) levels moved into a reusable object
  * with device-resident job tables -- a recorded circuit that can be replayed

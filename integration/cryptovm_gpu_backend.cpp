@@ -22,6 +22,9 @@ GpuBackend::GpuBackend(cvm_ctx* ctx, const cvm_keyset* owner, bool verify,
                        std::uint64_t enc_seed)
     : verify_(verify) {
   check(cvm_backend_create(ctx, owner, enc_seed, &gpu_), "cvm_backend_create");
+  // The reference decrypts words bit by bit (word.cpp:70-77): evaluate all
+  // pending gates at the first decrypt instead of one cone per bit.
+  check(cvm_backend_set_flush_policy(gpu_, CVM_FLUSH_ALL), "set_flush_policy");
   map_.push_back(0);  // node id 0 is the invalid handle
 }
 

@@ -263,6 +263,10 @@ class Backend:
     def flush(self):
         check(lib.cvm_backend_flush(self._h))
 
+    def set_flush_policy(self, policy):
+        """"cone" (default: decrypt/export evaluate only what they need) or "all"."""
+        check(lib.cvm_backend_set_flush_policy(self._h, {"cone": 0, "all": 1}[policy]))
+
     def capture_plan(self):
         h = ctypes.c_void_p()
         check(lib.cvm_backend_capture_plan(self._h, ctypes.byref(h)))

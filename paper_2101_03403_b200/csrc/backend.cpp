@@ -322,7 +322,8 @@ Plan* GpuBackend::capture_plan() {
 
 void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
   for (size_t i = 0; i < count; ++i) node(hs[i], "export");
-  flush_for(count, hs);
+  if (cone_only_) flush_for(count, hs);
+  else flush();
   std::lock_guard<std::mutex> lock(mu_);
   // Download the covering slot range in runs, then apply the linear forms.
   std::vector<int64_t> slots;

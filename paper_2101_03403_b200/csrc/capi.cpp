@@ -391,6 +391,14 @@ int cvm_backend_flush(cvm_backend* b) {
     if (b->gpu) b->gpu->flush();
   });
 }
+int cvm_backend_set_flush_policy(cvm_backend* b, int policy) {
+  return guard([&] {
+    need(b, "backend");
+    if (policy != CVM_FLUSH_CONE && policy != CVM_FLUSH_ALL)
+      throw InputError("unknown flush policy");
+    if (b->gpu) b->gpu->set_cone_only(policy == CVM_FLUSH_CONE);
+  });
+}
 int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out) {
   return guard([&] {
     need(b, "backend");

@@ -155,6 +155,10 @@ class GpuBackend final : public Backend {
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
   void flush();                             // everything pending
   void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only
+  // Flush policy of decrypt/export: the requested cone only (default) or
+  // everything pending (for callers that decrypt bit by bit, like the
+  // reference's decrypt_word loop, word.cpp:70-77).
+  void set_cone_only(bool on) { cone_only_ = on; }
   Plan* capture_plan();
   cvm_backend_stats stats() const;
   const std::vector<Node>& nodes() const { return nodes_; }
@@ -183,6 +187,7 @@ class GpuBackend final : public Backend {
   std::vector<cvm_gate> gates_;     // every recorded gate (node.gate_idx)
   std::vector<Bit> pending_;        // not yet evaluated gate nodes, id order
   uint64_t first_pending_ = UINT64_MAX;
+  bool cone_only_ = true;
   std::vector<std::string> regions_;
   uint64_t fences_ = 0;
   cvm_backend_stats stats_{};
