@@ -471,7 +471,15 @@ __device__ __forceinline__ void exchange_pair(c64 va[8], c64 vb[8], c64* ba, c64
 // (lane = 8*g + t%8), so the key-row loads of a warp hit 8 distinct
 // addresses (broadcast across gates) instead of 32; gates then advance in
 // CTA-wide lockstep (bar.sync 0 over 256 threads).
-template <int G, int S, bool kTwS = false, bool kIL = false>
+// biased gadget digit u = d + Bg/2 in [0,127] -> double d: bit-pattern
+// construction (no conversion unit, costs a register move) or I2F.
+template <bool kI2F>
+__device__ __forceinline__ double digit_to_double(uint32_t u) {
+  if constexpr (kI2F) return (double)(int)(u - 64u);
+  else return u32_biased_to_double(u, kDigitBias);
+}
+
+template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false>
 __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -566,10 +574,10 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
         const uint32_t da1 = ra1 - acc0[j + 512] + kDecompOffset;
         const uint32_t db0 = rb0 - acc1[j] + kDecompOffset;
         const uint32_t db1 = rb1 - acc1[j + 512] + kDecompOffset;
-        va[x] = {u32_biased_to_double((da0 >> shift) & 127u, kDigitBias),
-                 u32_biased_to_double((da1 >> shift) & 127u, kDigitBias)};
-        vb[x] = {u32_biased_to_double((db0 >> shift) & 127u, kDigitBias),
-                 u32_biased_to_double((db1 >> shift) & 127u, kDigitBias)};
+        va[x] = {digit_to_double<kI2F>((da0 >> shift) & 127u),
+                 digit_to_double<kI2F>((da1 >> shift) & 127u)};
+        vb[x] = {digit_to_double<kI2F>((db0 >> shift) & 127u),
+                 digit_to_double<kI2F>((db1 >> shift) & 127u)};
       }
       fwd_stage1(va, T1);
       fwd_stage1(vb, T1);
@@ -983,12 +991,12 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTwS = false, bool kIL = false>
+template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S, kTwS>));
-  auto* kern = blind_rotate_kernel_v3<G, S, kTwS, kIL>;
+  auto* kern = blind_rotate_kernel_v3<G, S, kTwS, kIL, kI2F>;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1048,6 +1056,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 3144: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3244: return launch_v3<4, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3344: return launch_v3<4, 4, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3444:
+      return launch_v3<4, 4, false, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
