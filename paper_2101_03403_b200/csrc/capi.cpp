@@ -231,7 +231,7 @@ int cvm_ctx_sm_count(cvm_ctx* c, int* sms) {
 int cvm_set_br_variant(int v) {
   return guard([&] {
     static const int known[] = {0,    1,    9,   22,  23,  43,   13,   123,  1233, 143,
-                                1432, 2233, 322, 640, 3044, 3045, 3024, 3144, 3244, 3344, 3444, 631, 531, 530};
+                                1432, 2233, 322, 640, 3044, 3045, 3024, 3144, 3244, 3344, 3444, 3544, 3644, 3744, 631, 531, 530};
     bool ok = false;
     for (int k : known) ok = ok || k == v;
     if (!ok)

@@ -479,7 +479,8 @@ __device__ __forceinline__ double digit_to_double(uint32_t u) {
   else return u32_biased_to_double(u, kDigitBias);
 }
 
-template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false>
+template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false,
+          int kShift = 0>
 __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -549,6 +550,16 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     }
   }
 
+  if constexpr (kShift > 0) {
+    // Offset gates 2,3 (which share SM sub-partitions with gates 0,1) by a
+    // fraction of a transform stage, so one gate's FP64 phase overlaps the
+    // other's shared-memory exchange instead of contending for the same pipe.
+    if (g >= 2) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < kShift) {
+      }
+    }
+  }
   int q = 0;  // chunk sequence number (pair order)
   for (int i = 0; i < kN; ++i) {
     group_sync_code(bar_id);
@@ -991,12 +1002,13 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false>
+template <int G, int S, bool kTwS = false, bool kIL = false, bool kI2F = false,
+          int kShift = 0>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S, kTwS>));
-  auto* kern = blind_rotate_kernel_v3<G, S, kTwS, kIL, kI2F>;
+  auto* kern = blind_rotate_kernel_v3<G, S, kTwS, kIL, kI2F, kShift>;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1058,6 +1070,15 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 3344: return launch_v3<4, 4, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3444:
       return launch_v3<4, 4, false, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 3544:
+      return launch_v3<4, 4, false, false, false, 400>(jobs, count, slab, bkf, tw1, tw2, xout,
+                                                       s);
+    case 3644:
+      return launch_v3<4, 4, false, false, false, 1200>(jobs, count, slab, bkf, tw1, tw2, xout,
+                                                        s);
+    case 3744:
+      return launch_v3<4, 4, false, false, false, 3000>(jobs, count, slab, bkf, tw1, tw2, xout,
+                                                        s);
     default: return cudaErrorInvalidValue;
   }
 }
