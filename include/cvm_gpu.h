@@ -142,14 +142,15 @@ CVM_API int cvm_ctx_fp64_peak(cvm_ctx* ctx, int reps, double* tflops);
 CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
 /* Blind-rotation kernel variant (process-wide): 1 = one bootstrap per CTA with
  * the key read through L1; 10*G+S = G bootstraps per CTA sharing an S-stage
- * bulk-copy shared-memory key ring (22, 23, 43, 13); 30GS = two transforms in
- * flight per thread (3044).  0 = auto (default): one bootstrap per CTA for
- * narrow levels, 3044 for wide ones.  Every
- * variant computes bit-identical ciphertexts. */
+ * bulk-copy shared-memory key ring (13, 22, 23, 43); 3044 = four bootstraps
+ * per CTA, two transforms in flight per thread; 9 = one bootstrap on 384
+ * threads (six gadget rows concurrently, latency).  0 = auto (default): 9 for
+ * levels up to 148 bootstraps, 13 up to 296, else 3044.  Every variant
+ * computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
-/* Key-switch kernel variant: 1 = one gate per CTA; 4/8 = gates per CTA
- * sharing each digit position's three non-zero KSK rows.  Bit-identical. */
+/* Key-switch kernel variant: 1 = one gate per CTA; 6 = one gate on 948
+ * threads (6 position groups, latency); 0 = auto (default).  Bit-identical. */
 CVM_API int cvm_set_ks_variant(int variant);
 CVM_API int cvm_get_ks_variant(void);
 

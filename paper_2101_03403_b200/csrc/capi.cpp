@@ -230,11 +230,7 @@ int cvm_ctx_sm_count(cvm_ctx* c, int* sms) {
 
 int cvm_set_br_variant(int v) {
   return guard([&] {
-    static const int known[] = {0,    1,    9,   22,  23,  43,   13,   123,  1233, 143,
-                                1432, 2233, 322, 640, 3044, 3045, 3024, 3144, 3244, 3344, 3444, 3544, 3644, 3744, 631, 531, 530};
-    bool ok = false;
-    for (int k : known) ok = ok || k == v;
-    if (!ok)
+    if (!cvm::valid_br_variant(v))
       throw InputError("unknown blind-rotation kernel variant " + std::to_string(v));
     cvm::set_br_variant(v);
   });
@@ -242,7 +238,7 @@ int cvm_set_br_variant(int v) {
 int cvm_get_br_variant(void) { return cvm::br_variant(); }
 int cvm_set_ks_variant(int v) {
   return guard([&] {
-    if (v != 0 && v != 1 && v != 4 && v != 6 && v != 8)
+    if (!cvm::valid_ks_variant(v))
       throw InputError("unknown key-switch kernel variant " + std::to_string(v));
     cvm::set_ks_variant(v);
   });

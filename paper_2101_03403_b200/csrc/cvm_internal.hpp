@@ -268,6 +268,8 @@ namespace cvm {
 int br_variant();
 void set_br_variant(int v);
 int default_br_variant();
+bool valid_br_variant(int v);
 int ks_variant();
 void set_ks_variant(int v);
+bool valid_ks_variant(int v);
 }  // namespace cvm

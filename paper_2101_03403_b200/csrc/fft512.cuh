@@ -113,16 +113,9 @@ CVM_HD int xpos(int cell, int slot) {
   return cell * 8 + ((slot ^ cell ^ (cell >> 3)) & 7);
 }
 
-// Twiddles held in shared memory as tw[k][thread] (thread-contiguous, so a
-// warp's 16-byte loads are bank-conflict-free); indexable like an array.
-struct StridedTw {
-  const c64* p;  // &tw[0][t]
-  CVM_HD c64 operator[](int k) const { return p[k * 64]; }
-};
-
 // ---------------------------------------------------------------- forward --
 // Input: v[a] = p_{t+64a} + i p_{t+64a+512} (untwisted).
-// TW: c64[8] (registers) or StridedTw (shared memory).
+// TW: anything indexable by k = 0..7 (the kernels pass register arrays).
 template <class TW>
 CVM_HD void fwd_stage1(c64 v[8], const TW& T1) {
 #pragma unroll

@@ -34,19 +34,21 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 uint32_t* xout, cudaStream_t s);
-// Blind-rotation kernel variant: 1 = one bootstrap per 64-thread CTA, key via
-// L1 (__ldg); 10*G + S = G bootstraps per CTA, key streamed through S
-// bulk-copy shared-memory stages.  Env CVM_BR_KERNEL overrides the default.
-constexpr int kDefaultBrVariant = 0;  // 0 = auto by level width
+// Blind-rotation kernel variant: 1 = v1 (one bootstrap per 64-thread CTA, key
+// via L1); 10*G + S = v2 (G bootstraps per CTA, S-stage bulk-copy key ring:
+// 13, 22, 23, 43); 3044 = v3 (G=4, S=4, two transforms per thread);
+// 9 = wide latency kernel.  0 = auto by level width (default).  Env
+// CVM_BR_KERNEL overrides the default.
+constexpr int kDefaultBrVariant = 0;
 int br_variant();
 void set_br_variant(int v);
-// Key-switch kernel: 1 = one gate per CTA; GK = 4/8/16 gates per CTA sharing
-// the three non-zero KSK rows of every digit position.  Env CVM_KS_KERNEL.
-// 0 = auto: 6 (one gate per 948-thread CTA, 6 position groups) for narrow
-// levels, 1 for wide ones (measured fastest there, profiles/).
+bool valid_br_variant(int v);
+// Key-switch kernel: 1 = one gate per CTA; 6 = one gate per 948-thread CTA
+// (6 position groups, latency); 0 = auto by level width.  Env CVM_KS_KERNEL.
 constexpr int kDefaultKsVariant = 0;
 int ks_variant();
 void set_ks_variant(int v);
+bool valid_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, uint32_t* slab, cudaStream_t s);

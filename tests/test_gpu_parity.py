@@ -45,7 +45,7 @@ def test_nand_level_bit_exact(keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), 1 - (a & b))
 
 
-@pytest.mark.parametrize("variant", [1, 9, 13, 22, 23, 43, 3024, 3044, 3045, 3244, 3344])
+@pytest.mark.parametrize("variant", [1, 9, 13, 22, 23, 43, 3044])
 def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     """Every blind-rotation kernel variant (one gate per CTA via L1, G gates per
     CTA on a bulk-copy shared-memory key ring) gives the oracle's ciphertexts,
@@ -73,7 +73,7 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
-@pytest.mark.parametrize("ks_variant", [1, 4, 6, 8])
+@pytest.mark.parametrize("ks_variant", [1, 6])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
     (two extracted samples + 1/8) and a partially filled last CTA."""
