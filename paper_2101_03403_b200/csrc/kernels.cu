@@ -847,7 +847,9 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
   if (count <= 0) return cudaSuccess;
   const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
   int variant = ks_variant();
-  if (variant == 0) variant = count <= 2 * 148 ? 6 : 1;  // auto by level width
+  // auto: the 6-group kernel is 10x faster on narrow levels and no slower on
+  // wide ones (profiles/r01_variant_sweep.txt)
+  if (variant == 0) variant = 6;
   switch (variant) {
     case 1: key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab); break;
     case 6:
