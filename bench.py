@@ -396,14 +396,14 @@ def run_ours(args):
         return 0
     extras = extra_configs(P, ctx, ks) if (ws == 1 and not args.no_extras) else None
     cpu = cpu_baseline() if (ws == 1 and not args.no_cpu) else None
+    # DRAM bytes per blind-rotation launch of this workload, from the committed
+    # ncu capture of the same command (profiles/ncu_blind_rotate.json)
     traffic = None
     prof = os.path.join(REPO, "profiles", "ncu_blind_rotate.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            traffic = pj["dram_bytes_per_bootstrap"] * boots_step / max(1, kst["br_launches"] /
-                                                                       args.steps)
-        except Exception:
+            traffic = json.load(open(prof))["blind_rotate_v3"]["avg_dram_bytes_per_launch"]
+        except (KeyError, ValueError):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "bootstrapped gates/s", "n_gpus": ws,
@@ -425,6 +425,9 @@ def run_ours(args):
         "roofline": {"bound": "fp64", "kernel": "blind_rotate_kernel",
                      "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per blind_rotate launch (ncu)",
+                     "algorithmic_bytes_per_launch": 61_931_520 + (2524 + 4112) * boots_step
+                     / max(1.0, kst["br_launches"] / args.steps),
                      "peak_source": "DFMA peak measured live in bench.py (cvm_ctx_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
                      "algorithmic_flop_per_bootstrap": ALG_FLOP_PER_BOOTSTRAP},
