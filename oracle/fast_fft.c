@@ -4,10 +4,17 @@
  *
  * This is the TFHE library's own method for the external product (a real
  * polynomial mod X^N+1 folded into N/2 complex points, twisted by the 2N-th
- * root of unity, one N/2-point complex FFT), restated as an iterative radix-2
- * FFT on split real/imaginary arrays with contiguous per-stage twiddles so the
- * compiler vectorises the butterflies (AVX2 with -march=x86-64-v3).
- * N = 1024, M = N/2 = 512.  Spectra are stored split: re[0..511], im[0..511].
+ * root of unity, one N/2-point complex FFT), restated on split real/imaginary
+ * arrays so the compiler vectorises the butterflies (AVX2 with
+ * -march=x86-64-v3):
+ *   forward = twist + decimation-in-frequency radix-2 (natural in,
+ *             bit-reversed out), last two stages fused into a multiply-free
+ *             radix-4 pass;
+ *   inverse = the mirror decimation-in-time pass (bit-reversed in, natural
+ *             out) + untwist.
+ * Point-wise products do not care about bin order, so no bit reversal is ever
+ * performed.  N = 1024, M = N/2 = 512.  Spectra are stored split:
+ * re[0..511], im[0..511].
  */
 #include <math.h>
 #include <pthread.h>
@@ -17,9 +24,8 @@
 #define N 1024
 #define M 512
 
-static double tw_re[M], tw_im[M];   /* fold twist omega^j = e^{i pi j / N}        */
-static double st_re[M], st_im[M];   /* stage twiddles: [h + j] = e^{-i pi j / h}  */
-static int rev9[M];
+static double tw_re[M], tw_im[M];  /* fold twist omega^j = e^{i pi j / N}       */
+static double st_re[M], st_im[M];  /* stage twiddles: [h + j] = e^{-i pi j / h} */
 static pthread_once_t once = PTHREAD_ONCE_INIT;
 
 static void init(void) {
@@ -32,31 +38,14 @@ static void init(void) {
       st_re[h + j] = cos(M_PI * j / h);
       st_im[h + j] = -sin(M_PI * j / h);
     }
-  for (int i = 0; i < M; ++i) {
-    int r = 0;
-    for (int b = 0; b < 9; ++b)
-      if (i & (1 << b)) r |= 1 << (8 - b);
-    rev9[i] = r;
-  }
 }
 
 void ff_init(void) { pthread_once(&once, init); }
 
-/* In-place DIT FFT on split arrays; inverse uses conjugate twiddles (unscaled). */
-static void fft512(double* restrict re, double* restrict im, int inverse) {
-  for (int i = 0; i < M; ++i) {
-    const int r = rev9[i];
-    if (i < r) {
-      double t = re[i];
-      re[i] = re[r];
-      re[r] = t;
-      t = im[i];
-      im[i] = im[r];
-      im[r] = t;
-    }
-  }
-  const double sgn = inverse ? -1.0 : 1.0;
-  for (int h = 1; h < M; h <<= 1) {
+/* Forward DIF, stages h = 256 .. 4 with twiddles, then a fused radix-4 pass
+ * for h = 2 (twiddles 1, -i) and h = 1 (twiddle 1). */
+static void fft_dif(double* restrict re, double* restrict im) {
+  for (int h = M / 2; h >= 4; h >>= 1) {
     const double* wr = st_re + h;
     const double* wi = st_im + h;
     for (int i = 0; i < M; i += 2 * h) {
@@ -65,13 +54,68 @@ static void fft512(double* restrict re, double* restrict im, int inverse) {
       double* vr = re + i + h;
       double* vi = im + i + h;
       for (int j = 0; j < h; ++j) {
-        const double c = wr[j], s = sgn * wi[j];
-        const double xr = vr[j] * c - vi[j] * s;
-        const double xi = vr[j] * s + vi[j] * c;
-        vr[j] = ur[j] - xr;
-        vi[j] = ui[j] - xi;
-        ur[j] += xr;
-        ui[j] += xi;
+        const double ar = ur[j] - vr[j], ai = ui[j] - vi[j];
+        ur[j] += vr[j];
+        ui[j] += vi[j];
+        vr[j] = ar * wr[j] - ai * wi[j];
+        vi[j] = ar * wi[j] + ai * wr[j];
+      }
+    }
+  }
+  for (int i = 0; i < M; i += 4) {
+    const double x0r = re[i], x1r = re[i + 1], x2r = re[i + 2], x3r = re[i + 3];
+    const double x0i = im[i], x1i = im[i + 1], x2i = im[i + 2], x3i = im[i + 3];
+    /* h = 2: (x0,x2), (x1,x3)*(-i) on the difference */
+    const double a0r = x0r + x2r, a0i = x0i + x2i, a2r = x0r - x2r, a2i = x0i - x2i;
+    const double a1r = x1r + x3r, a1i = x1i + x3i;
+    const double d3r = x1r - x3r, d3i = x1i - x3i;
+    const double a3r = d3i, a3i = -d3r; /* times -i */
+    /* h = 1 */
+    re[i] = a0r + a1r;
+    im[i] = a0i + a1i;
+    re[i + 1] = a0r - a1r;
+    im[i + 1] = a0i - a1i;
+    re[i + 2] = a2r + a3r;
+    im[i + 2] = a2i + a3i;
+    re[i + 3] = a2r - a3r;
+    im[i + 3] = a2i - a3i;
+  }
+}
+
+/* Inverse DIT (conjugate twiddles, unscaled): the exact mirror of fft_dif. */
+static void fft_dit_inv(double* restrict re, double* restrict im) {
+  for (int i = 0; i < M; i += 4) {
+    const double y0r = re[i], y1r = re[i + 1], y2r = re[i + 2], y3r = re[i + 3];
+    const double y0i = im[i], y1i = im[i + 1], y2i = im[i + 2], y3i = im[i + 3];
+    /* h = 1 */
+    const double a0r = y0r + y1r, a0i = y0i + y1i, a1r = y0r - y1r, a1i = y0i - y1i;
+    const double a2r = y2r + y3r, a2i = y2i + y3i, e3r = y2r - y3r, e3i = y2i - y3i;
+    /* h = 2: second of each pair times +i */
+    const double a3r = -e3i, a3i = e3r;
+    re[i] = a0r + a2r;
+    im[i] = a0i + a2i;
+    re[i + 2] = a0r - a2r;
+    im[i + 2] = a0i - a2i;
+    re[i + 1] = a1r + a3r;
+    im[i + 1] = a1i + a3i;
+    re[i + 3] = a1r - a3r;
+    im[i + 3] = a1i - a3i;
+  }
+  for (int h = 4; h < M; h <<= 1) {
+    const double* wr = st_re + h;
+    const double* wi = st_im + h;
+    for (int i = 0; i < M; i += 2 * h) {
+      double* ur = re + i;
+      double* ui = im + i;
+      double* vr = re + i + h;
+      double* vi = im + i + h;
+      for (int j = 0; j < h; ++j) {
+        const double br = vr[j] * wr[j] + vi[j] * wi[j];  /* v * conj(w) */
+        const double bi = vi[j] * wr[j] - vr[j] * wi[j];
+        vr[j] = ur[j] - br;
+        vi[j] = ui[j] - bi;
+        ur[j] += br;
+        ui[j] += bi;
       }
     }
   }
@@ -85,7 +129,7 @@ static void forward_d(const double* p, double* out) {
     re[j] = x * tw_re[j] - y * tw_im[j];
     im[j] = x * tw_im[j] + y * tw_re[j];
   }
-  fft512(re, im, 0);
+  fft_dif(re, im);
 }
 
 void ff_forward_int(const int32_t* in, double* out) {
@@ -104,7 +148,7 @@ void ff_inverse_round(const double* in, uint32_t* out) {
   double re[M], im[M];
   memcpy(re, in, sizeof(re));
   memcpy(im, in + M, sizeof(im));
-  fft512(re, im, 1);
+  fft_dit_inv(re, im);
   const double s = 1.0 / M;
   for (int j = 0; j < M; ++j) {
     const double zr = re[j] * s, zi = im[j] * s;
