@@ -825,8 +825,23 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   if (variant == 0) {
     // auto: a narrow level runs each bootstrap on a whole SM (latency); a
     // level of up to two bootstraps per SM gives each its own CTA; wide
-    // levels use the throughput kernel.
-    variant = count <= 148 ? 9 : count <= 2 * 148 ? 13 : 3044;
+    // levels use the throughput kernel, whose SMs work in rounds of 4
+    // bootstraps (~6.6 ms).  A last partial round of at most 2 bootstraps per
+    // SM is cheaper on the latency kernel (2 x 2.3 ms), so it is split off.
+    constexpr int kSms = 148, kRound = 4 * kSms;
+    if (count <= kSms) {
+      variant = 9;
+    } else if (count <= 2 * kSms) {
+      variant = 13;
+    } else {
+      const int tail = count % kRound;
+      if (tail > 0 && tail <= 2 * kSms && count > kRound) {
+        cudaError_t e = launch_v3<4, 4>(jobs, count - tail, slab, bkf, tw1, tw2, xout, s);
+        if (e != cudaSuccess) return e;
+        return launch_wide(jobs + (count - tail), tail, slab, bkf, tw1, tw2, xout, s);
+      }
+      variant = 3044;
+    }
   }
   switch (variant) {
     case 1:
