@@ -240,7 +240,6 @@ def extra_configs(P, ctx, ks):
     vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
     d["correct"] = bool(np.array_equal(vals, (av << (bv % WIDTH)) % (1 << WIDTH)))
     out["config3_lsl16"] = d
-    # config 4: 64 x MUL16 (low 16 bits used by the emulator)
     # config 4: 64 x MUL16 producing the low 16 bits (the emulator's MUL):
     # the high half's 2,083 gates per multiplier are dead and never run
     av, bv, res, d = fu("mul_lo", 64, 930)

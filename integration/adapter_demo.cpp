@@ -3,6 +3,7 @@
 // cryptovm::GpuBackend, with verify=true so every decryption is also checked
 // against the shadow SimBackend.  Exit code 0 = all results correct.
 #include <cstdio>
+#include <filesystem>
 #include <memory>
 #include <random>
 
@@ -11,6 +12,8 @@
 #include "cryptovm/isa.hpp"
 #include "cryptovm/keyservice.hpp"
 #include "cryptovm/word.hpp"
+#include "cryptovm/errors.hpp"
+#include "cryptovm_ct_image.hpp"
 #include "cryptovm_gpu_backend.hpp"
 
 using namespace cryptovm;
@@ -67,6 +70,42 @@ int main() {
     bad += !ok;
     std::printf("machine 13*11 loop: R0=%llu branches=%llu %s\n", (unsigned long long)r0,
                 (unsigned long long)m.stats().branch_queries, ok ? "ok" : "FAIL");
+    // 4) ciphertext-sized memory image + NZCV branch payload (SURVEY f-2):
+    //    the emulator LOADs/STOREs 2,524-B LWE blobs through the image file,
+    //    and a branch query carrying the four flag ciphertexts is resolved.
+    {
+      const std::string path =
+          (std::filesystem::temp_directory_path() / "cvm_ct_image_demo.bin").string();
+      encrypt_ct_file(bk, {5, 9, 1000, 0xFFFF}, 16, path);
+      LocalBranchOracle oracle2(bk);
+      auto mem = std::make_unique<CiphertextFileMemory>(bk, path);
+      const std::size_t blob = mem->blob_bytes();
+      Machine m2(bk, {.word_size = 16}, std::move(mem), oracle2);
+      m2.run(assemble(".word_size 16\nLOAD R0 0\nLOAD R1 1\nADD R2 R0 R1\nSTORE R2 3\n"
+                      "LOAD R3 2\nSUBS R4 R3 R0\nSTORE R4 0\nHALT\n"),
+             100);
+      const MemoryImage img = decrypt_ct_file(bk, path);
+      bool ok = blob == CVM_LWE_WORDS * 4 && img.width == 16 &&
+                img.values == std::vector<std::uint64_t>{995, 9, 1000, 14};
+      BranchQuery q;
+      q.cond = CondCode::Hi;  // unsigned higher: C set and Z clear (1000 > 5)
+      q.nzcv_payload = serialize_flags(bk, m2.flags());
+      q.target = 7;
+      q.fallthrough = 3;
+      const BranchReply r = resolve_branch_ct(q, bk, /*user_controlled=*/true);
+      ok = ok && q.nzcv_payload.size() == 4 * blob && r.next_pc == 7u;
+      bool rejected = false;
+      try {
+        resolve_branch(q, bk);  // the reference's 1-byte-per-flag check
+      } catch (const ProtocolError&) {
+        rejected = true;
+      }
+      ok = ok && rejected;
+      std::filesystem::remove(path);
+      bad += !ok;
+      std::printf("ciphertext image + branch payload (%zu-B blobs): %s\n", blob,
+                  ok ? "ok" : "FAIL");
+    }
     const cvm_backend_stats st = bk.stats();
     std::printf("stats: nodes=%llu bootstrapped=%llu levels=%llu flushes=%llu mismatches=%llu\n",
                 (unsigned long long)st.nodes, (unsigned long long)st.bootstrapped,

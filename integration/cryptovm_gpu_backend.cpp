@@ -20,7 +20,7 @@ void check(int rc, const char* what) {
 
 GpuBackend::GpuBackend(cvm_ctx* ctx, const cvm_keyset* owner, bool verify,
                        std::uint64_t enc_seed)
-    : verify_(verify) {
+    : owner_(owner), verify_(verify) {
   check(cvm_backend_create(ctx, owner, enc_seed, &gpu_), "cvm_backend_create");
   // The reference decrypts words bit by bit (word.cpp:70-77): evaluate all
   // pending gates at the first decrypt instead of one cone per bit.
@@ -111,9 +111,16 @@ BitHandle GpuBackend::import_bit(const std::vector<std::uint8_t>& blob) {
   std::lock_guard<std::mutex> lock(mu_);
   cvm_handle g;
   check(cvm_backend_import_bit(gpu_, blob.data(), blob.size(), &g), "import_bit");
-  // The shadow records an input node; its clear bit is unknown to the
-  // evaluator, so it is left false (no plaintext enters the shadow).
-  return bind(shadow_.import_bit({0}), g);
+  // The shadow records an input node.  Only in verify mode (a test harness
+  // holding the owner key) does it learn the clear bit, so later decryptions
+  // of gates over imported bits can still be checked against it.
+  std::uint8_t clear = 0;
+  if (verify_) {
+    check(cvm_decrypt_bits(owner_, 1, reinterpret_cast<const uint32_t*>(blob.data()), &clear,
+                           nullptr),
+          "import_bit (verify)");
+  }
+  return bind(shadow_.import_bit({clear}), g);
 }
 
 void GpuBackend::push_region(std::string_view name) {

@@ -58,6 +58,7 @@ class GpuBackend final : public Backend {
 
   SimBackend shadow_;
   cvm_backend* gpu_ = nullptr;
+  const cvm_keyset* owner_;
   bool verify_;
   std::vector<cvm_handle> map_;  // shadow node id -> cvm handle
   std::uint64_t mismatches_ = 0;

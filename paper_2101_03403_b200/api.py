@@ -129,8 +129,10 @@ class Context:
         check(lib.cvm_download_lwe(self._h, slot, count, _vp(out)))
         return out
 
-    def submit_level(self, gates):
-        """gates: list of (kind, [(slot, sign, const), ...], out_slot)."""
+    @staticmethod
+    def pack_level(gates):
+        """gates: list of (kind, [(slot, sign, const), ...], out_slot) ->
+        the C `cvm_gate` array `submit_level` takes (pack once, submit many)."""
         arr = (N.Gate * len(gates))()
         for g, (kind, ins, out) in zip(arr, gates):
             g.kind = KIND[kind] if isinstance(kind, str) else kind
@@ -138,7 +140,12 @@ class Context:
                 s, sg, c = ins[i] if i < len(ins) else (-1, 1, 0)
                 g.inp[i].slot, g.inp[i].sign, g.inp[i].constant = s, sg, c & 0xFFFFFFFF
             g.out_slot = out
-        check(lib.cvm_submit_level(self._h, arr, len(gates)))
+        return arr
+
+    def submit_level(self, gates):
+        """gates: a gate list (see `pack_level`) or an already packed array."""
+        arr = gates if isinstance(gates, ctypes.Array) else self.pack_level(gates)
+        check(lib.cvm_submit_level(self._h, arr, len(arr)))
 
     def sync(self):
         check(lib.cvm_sync(self._h))

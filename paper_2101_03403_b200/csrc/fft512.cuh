@@ -41,6 +41,15 @@ CVM_HD c64 cmul_conj(c64 a, c64 b) {  // a * conj(b)
   return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
 }
 CVM_HD c64 cadd(c64 a, c64 b) { return {a.x + b.x, a.y + b.y}; }
+// acc + a * b as four FMAs (cadd(acc, cmul(a, b)) costs 2 MUL + 2 FMA + 2 ADD:
+// without reassociation the compiler cannot fold the accumulate).
+CVM_HD c64 cmac(c64 acc, c64 a, c64 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
 CVM_HD c64 csub(c64 a, c64 b) { return {a.x - b.x, a.y - b.y}; }
 
 // e^{i pi a / 16}, a = 0..7: the stride-64 part of the fold twist w^{64a}.

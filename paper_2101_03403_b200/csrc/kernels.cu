@@ -258,8 +258,8 @@ __global__ void __launch_bounds__(64) blind_rotate_kernel(
         const c64* bk_r = bk_i + (size_t)(part * kL + p) * 1024;
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          af[0][k2] = cadd(af[0][k2], cmul(v[k2], ldg_c64(bk_r + k2 * 128 + t)));
-          af[1][k2] = cadd(af[1][k2], cmul(v[k2], ldg_c64(bk_r + k2 * 128 + 64 + t)));
+          af[0][k2] = cmac(af[0][k2], v[k2], ldg_c64(bk_r + k2 * 128 + t));
+          af[1][k2] = cmac(af[1][k2], v[k2], ldg_c64(bk_r + k2 * 128 + 64 + t));
         }
       }
     }
@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
         const c64* bk_r = sm.ring[slot];
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          af[0][k2] = cadd(af[0][k2], cmul(v[k2], bk_r[k2 * 128 + t]));
-          af[1][k2] = cadd(af[1][k2], cmul(v[k2], bk_r[k2 * 128 + 64 + t]));
+          af[0][k2] = cmac(af[0][k2], v[k2], bk_r[k2 * 128 + t]);
+          af[1][k2] = cmac(af[1][k2], v[k2], bk_r[k2 * 128 + 64 + t]);
         }
         mbar_arrive(&sm.empty[slot]);
       }
@@ -501,8 +501,8 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
       for (int k2 = 0; k2 < 8; ++k2) {
         const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
         const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
-        af[0][k2] = cadd(cadd(af[0][k2], cmul(va[k2], a0)), cmul(vb[k2], b0));
-        af[1][k2] = cadd(cadd(af[1][k2], cmul(va[k2], a1)), cmul(vb[k2], b1));
+        af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
+        af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
       }
       mbar_arrive(&sm.empty[sa]);
       mbar_arrive(&sm.empty[sb]);
@@ -655,7 +655,8 @@ __global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
 #pragma unroll
     for (int j = 0; j < kKsT; ++j) {
       const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
-      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);  // d = 0 row is zero
+      if (d == 0) continue;  // the d = 0 rows are zero (uniform across the CTA)
+      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);
       a.x -= r.x;
       a.y -= r.y;
       a.z -= r.z;
@@ -696,6 +697,7 @@ __global__ void __launch_bounds__(kKsWideThreads) key_switch_wide_kernel(
 #pragma unroll
     for (int j = 0; j < kKsT; ++j) {
       const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
+      if (d == 0) continue;
       const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);
       a.x -= r.x;
       a.y -= r.y;
@@ -862,9 +864,10 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
   if (count <= 0) return cudaSuccess;
   const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
   int variant = ks_variant();
-  // auto: the 6-group kernel is 10x faster on narrow levels and no slower on
-  // wide ones (profiles/r01_variant_sweep.txt)
-  if (variant == 0) variant = 6;
+  // auto: the 6-group kernel is 10x faster on narrow levels; with the zero
+  // digit rows skipped the 1-group kernel is ~8% faster on wide ones
+  // (profiles/r01_variant_sweep.txt)
+  if (variant == 0) variant = count >= 1024 ? 1 : 6;
   switch (variant) {
     case 1: key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab); break;
     case 6:

@@ -19,3 +19,16 @@ def test_reference_alu_and_machine_run_on_gpu_backend():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ADAPTER OK" in r.stdout
     assert "mismatches=0" in r.stdout
+    assert "ciphertext image + branch payload (2524-B blobs): ok" in r.stdout
+
+
+CT_CHECK = os.path.join(REPO, "integration", "_build", "ct_image_check")
+
+
+@pytest.mark.skipif(not os.path.exists(CT_CHECK), reason="ct_image_check not built (needs /root/reference)")
+def test_ciphertext_image_on_reference_sim_backend():
+    """SURVEY f-2 on the CPU: ciphertext-sized memory images and NZCV payloads
+    with the reference SimBackend (1-B blobs), incl. the error paths."""
+    r = subprocess.run([CT_CHECK], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "CT IMAGE OK" in r.stdout
