@@ -150,7 +150,9 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
 /* Key-switch kernel variant: 1 = one gate per CTA; 6 = one gate on 948
- * threads (6 position groups, latency); 0 = auto (default).  Bit-identical. */
+ * threads (6 position groups, latency); 7 = the level as one INT8
+ * tensor-core product (one-hot digits x KSK byte limbs); 0 = auto (default:
+ * 6 below 768 gates, else 7).  Bit-identical. */
 CVM_API int cvm_set_ks_variant(int variant);
 CVM_API int cvm_get_ks_variant(void);
 

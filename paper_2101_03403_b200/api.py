@@ -366,7 +366,7 @@ def fu_batch(ctx, op, width, a_lwe, b_lwe, c_lwe=None):
     batch = a.size // (width * N.LWE_WORDS)
     c = _u32(c_lwe) if c_lwe is not None else None
     ow = lib.cvm_fu_out_width(opi, width)
-    out = np.zeros((batch, ow, N.LWE_WORDS), np.uint32)
+    out = np.empty((batch, ow, N.LWE_WORDS), np.uint32)
     st = N.BackendStats()
     check(lib.cvm_fu_batch(ctx.handle, opi, width, batch, _vp(a), _vp(b), _vp(c), _vp(out),
                            ctypes.byref(st)))

@@ -190,10 +190,47 @@ void GpuBackend::import_lwe(size_t count, const uint32_t* lwe, Bit* out) {
   }
 }
 
+// Zero-copy import for synchronous batch entry points (cvm_fu_batch): one
+// contiguous slot run uploaded straight from the caller's buffer (a direct
+// DMA when it is pinned, one staging copy otherwise).  The caller keeps `lwe`
+// alive until the context is synchronised.
+void GpuBackend::import_lwe_direct(size_t count, const uint32_t* lwe, Bit* out) {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (count == 0) return;
+  if (!lwe) throw InputError("import: null ciphertexts");
+  stage_uploads();  // keep earlier staged uploads ordered before this one
+  const uint64_t first = context_alloc_slots(ctx_, count);
+  runs_.push_back({first, first + count});
+  context_reserve(ctx_, context_slots_used(ctx_));
+  context_upload(ctx_, first, count, lwe);
+  for (size_t i = 0; i < count; ++i) {
+    Node n{};
+    n.kind = GateKind::Constant;
+    n.input = true;
+    n.slot = int64_t(first + i);
+    n.sign = 1;
+    out[i] = add_node(n);
+  }
+}
+
+bool GpuBackend::release_slots() {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (runs_.empty()) return true;
+  auto r = runs_;
+  std::sort(r.begin(), r.end());
+  for (size_t i = 1; i < r.size(); ++i)
+    if (r[i].first != r[i - 1].second) return false;  // another user interleaved
+  if (!context_release_slots(ctx_, r.front().first, r.back().second)) return false;
+  runs_.clear();
+  next_slot_ = chunk_end_ = 0;
+  return true;
+}
+
 uint64_t GpuBackend::take_slot() {
   if (next_slot_ == chunk_end_) {
     next_slot_ = context_alloc_slots(ctx_, chunk_);
     chunk_end_ = next_slot_ + chunk_;
+    runs_.push_back({next_slot_, chunk_end_});
     chunk_ = std::min<uint64_t>(chunk_ * 2, uint64_t(1) << 20);
   }
   return next_slot_++;
@@ -325,35 +362,29 @@ void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
   if (cone_only_) flush_for(count, hs);
   else flush();
   std::lock_guard<std::mutex> lock(mu_);
-  // Download the covering slot range in runs, then apply the linear forms.
-  std::vector<int64_t> slots;
-  for (size_t i = 0; i < count; ++i)
-    if (nodes_[hs[i] - 1].slot >= 0) slots.push_back(nodes_[hs[i] - 1].slot);
-  std::sort(slots.begin(), slots.end());
-  slots.erase(std::unique(slots.begin(), slots.end()), slots.end());
-  std::vector<uint32_t> buf;
-  std::vector<std::pair<int64_t, size_t>> where;  // slot -> offset in buf
-  size_t i = 0;
-  while (i < slots.size()) {
-    size_t j = i;
-    while (j + 1 < slots.size() && slots[j + 1] - slots[j] <= 16) ++j;
-    const uint64_t lo = uint64_t(slots[i]), n = uint64_t(slots[j] - slots[i] + 1);
-    const size_t off = buf.size();
-    buf.resize(off + n * kLweWords);
-    context_download(ctx_, lo, n, buf.data() + off);
-    for (size_t k = i; k <= j; ++k)
-      where.push_back({slots[k], off + size_t(slots[k] - slots[i]) * kLweWords});
-    i = j + 1;
-  }
+  // One device gather of the requested slots (in request order) and one
+  // download, then the linear forms (NOT / COPY / CONSTANT) applied on the host.
+  std::vector<uint64_t> sl;
+  sl.reserve(count);
+  for (size_t q = 0; q < count; ++q)
+    if (nodes_[hs[q] - 1].slot >= 0) sl.push_back(uint64_t(nodes_[hs[q] - 1].slot));
+  const bool direct = sl.size() == count;  // gather straight into `out`
+  std::vector<uint32_t> buf(direct ? 0 : sl.size() * kLweWords);
+  uint32_t* base = direct ? out : buf.data();
+  context_gather_download(ctx_, sl.data(), sl.size(), base);
+  size_t k = 0;
   for (size_t q = 0; q < count; ++q) {
     const Node& n = nodes_[hs[q] - 1];
     uint32_t* o = out + q * kLweWords;
     if (n.slot < 0) {
       std::memset(o, 0, kLweWords * 4);
     } else {
-      auto it = std::lower_bound(where.begin(), where.end(), std::make_pair(n.slot, size_t(0)));
-      const uint32_t* src = buf.data() + it->second;
-      for (int w = 0; w < kLweWords; ++w) o[w] = n.sign > 0 ? src[w] : 0u - src[w];
+      const uint32_t* src = base + (k++) * kLweWords;
+      if (n.sign > 0) {
+        if (src != o) std::memcpy(o, src, kLweWords * 4);
+      } else {
+        for (int w = 0; w < kLweWords; ++w) o[w] = 0u - src[w];
+      }
     }
     o[kN] += n.constant;
   }

@@ -1,6 +1,9 @@
 // extern "C" wrappers (include/cvm_gpu.h).  Exceptions become status codes
 // and a thread-local message, mirroring the reference's InputError / Error
 // split (errors.hpp:24-58).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -498,20 +501,40 @@ int cvm_fu_batch(cvm_ctx* c, uint32_t op, uint32_t width, uint64_t batch, const 
     if (ow < 0) throw InputError("unknown functional-unit op");
     const bool uses_c = op == CVM_FU_ADD_CIN || op == CVM_FU_ADDSUB;
     if (uses_c) need(c_lwe, "c");
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     GpuBackend bk(c->ctx, nullptr, 0);
     std::vector<Bit> ha(batch * width), hb(batch * width), hc(uses_c ? batch : 0);
-    bk.import_lwe(ha.size(), a_lwe, ha.data());
-    bk.import_lwe(hb.size(), b_lwe, hb.data());
-    if (uses_c) bk.import_lwe(hc.size(), c_lwe, hc.data());
-    std::vector<Bit> outs;
-    outs.reserve(batch * size_t(ow));
-    for (uint64_t i = 0; i < batch; ++i) {
-      Word r = fu_apply(bk, op, Word(&ha[i * width], &ha[i * width] + width),
-                        Word(&hb[i * width], &hb[i * width] + width), uses_c ? hc[i] : 0);
-      outs.insert(outs.end(), r.begin(), r.end());
+    // Inputs are DMA'd straight from the caller's buffers; every path out of
+    // this call synchronises the stream first, so they may be released after.
+    auto t1 = t0, t2 = t0;
+    try {
+      bk.import_lwe_direct(ha.size(), a_lwe, ha.data());
+      bk.import_lwe_direct(hb.size(), b_lwe, hb.data());
+      if (uses_c) bk.import_lwe_direct(hc.size(), c_lwe, hc.data());
+      t1 = clk::now();
+      std::vector<Bit> outs;
+      outs.reserve(batch * size_t(ow));
+      for (uint64_t i = 0; i < batch; ++i) {
+        Word r = fu_apply(bk, op, Word(&ha[i * width], &ha[i * width] + width),
+                          Word(&hb[i * width], &hb[i * width] + width), uses_c ? hc[i] : 0);
+        outs.insert(outs.end(), r.begin(), r.end());
+      }
+      t2 = clk::now();
+      bk.export_lwe(outs.size(), outs.data(), out_lwe);  // synchronises
+      bk.release_slots();  // the batch's slots are scratch: reuse them next call
+    } catch (...) {
+      context_sync(c->ctx);
+      throw;
     }
-    bk.export_lwe(outs.size(), outs.data(), out_lwe);
     if (stats) *stats = bk.stats();
+    if (std::getenv("CVM_FU_TIMING")) {
+      const auto ms = [](auto a, auto b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+      };
+      std::fprintf(stderr, "cvm_fu_batch: import %.2f ms, record %.2f ms, run+export %.2f ms\n",
+                   ms(t0, t1), ms(t1, t2), ms(t2, clk::now()));
+    }
   });
 }
 

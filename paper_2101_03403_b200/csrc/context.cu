@@ -102,6 +102,7 @@ class Context {
     cudaFree(tw2_);
     cudaFree(bkf_);
     cudaFree(ksk_);
+    cudaFree(kskb_);
     cudaFree(slab_);
     cudaFree(xlwe_);
     cudaFree(flush_buf_);
@@ -125,6 +126,9 @@ class Context {
     check(cudaMemcpy2DAsync(ksk_, kKskRowStride * 4, ksk, kLweWords * 4, kLweWords * 4,
                             ksk_rows, cudaMemcpyHostToDevice, stream_),
           "upload ksk");
+    if (!kskb_) check(cudaMalloc(&kskb_, kKskbWords * 4), "cudaMalloc(kskb)");
+    check(launch_ksk_to_limbs(ksk_, kskb_, stream_), "ksk_to_limbs");
+    ++stats_.other_launches;
     check(cudaStreamSynchronize(stream_), "sync(upload_keys)");
     cudaFree(bk_tmp);
     has_keys_ = true;
@@ -158,6 +162,15 @@ class Context {
     return base;
   }
   uint64_t slots_used() const { return used_; }
+  // Return the top run [first, end) to the allocator if nothing was handed out
+  // after it (stack discipline; a temporary backend's slots after its work
+  // has been synchronised).
+  bool release_slots(uint64_t first, uint64_t end) {
+    std::lock_guard<std::mutex> lock(alloc_mu_);
+    if (end != used_ || first > end) return false;
+    used_ = first;
+    return true;
+  }
 
   void upload(uint64_t slot, uint64_t count, const uint32_t* lwe) {
     if (count == 0) return;
@@ -186,6 +199,35 @@ class Context {
     check(cudaMemcpy2DAsync(lwe, kLweWords * 4, slab_ + slot * kLweStride, kLweStride * 4,
                             kLweWords * 4, count, cudaMemcpyDeviceToHost, stream_),
           "download_lwe");
+    sync();
+  }
+
+  // Download an arbitrary slot list as one contiguous [count][631] block: a
+  // device gather into the arena, one D2H copy (straight into `lwe` when it
+  // is pinned), one synchronisation.
+  void gather_download(const uint64_t* slots, uint64_t count, uint32_t* lwe) {
+    if (count == 0) return;
+    if (!lwe || !slots) throw InputError("gather_download: null pointer");
+    for (uint64_t i = 0; i < count; ++i)
+      if (slots[i] >= cap_) throw InputError("gather_download: slot beyond capacity");
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const size_t bytes = count * kLweWords * 4;
+    uint64_t* h_slots = static_cast<uint64_t*>(host_arena_.alloc(count * 8));
+    std::memcpy(h_slots, slots, count * 8);
+    uint64_t* d_slots = static_cast<uint64_t*>(dev_arena_.alloc(count * 8));
+    uint32_t* d_out = static_cast<uint32_t*>(dev_arena_.alloc(bytes));
+    check(cudaMemcpyAsync(d_slots, h_slots, count * 8, cudaMemcpyHostToDevice, stream_),
+          "upload gather slots");
+    check(launch_gather_lwe(slab_, d_slots, count, d_out, stream_), "gather_lwe");
+    ++stats_.other_launches;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, lwe) == cudaSuccess &&
+                        attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    void* dst = pinned ? static_cast<void*>(lwe) : host_arena_.alloc(bytes);
+    check(cudaMemcpyAsync(dst, d_out, bytes, cudaMemcpyDeviceToHost, stream_), "download");
+    check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+    if (!pinned) std::memcpy(lwe, dst, bytes);
     sync();
   }
 
@@ -231,7 +273,7 @@ class Context {
           "blind_rotate_kernel");
     end_prof(p);
     p = begin_prof(1);
-    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, slab_, stream_),
+    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, slab_, stream_),
           "key_switch_kernel");
     end_prof(p);
     stats_.br_launches++;
@@ -459,6 +501,7 @@ class Context {
   cudaStream_t stream_ = nullptr;
   c64 *tw1_ = nullptr, *tw2_ = nullptr, *bkf_ = nullptr;
   uint32_t* ksk_ = nullptr;
+  uint32_t* kskb_ = nullptr;  // KSK as byte limbs for the tensor-core key switch
   uint32_t* slab_ = nullptr;
   uint64_t cap_ = 0;
   uint64_t used_ = 0;
@@ -484,11 +527,18 @@ void context_reserve(Context* c, uint64_t n) { c->reserve(n); }
 uint64_t context_capacity(const Context* c) { return c->capacity(); }
 uint64_t context_alloc_slots(Context* c, uint64_t n) { return c->alloc_slots(n); }
 uint64_t context_slots_used(const Context* c) { return c->slots_used(); }
+bool context_release_slots(Context* c, uint64_t first, uint64_t end) {
+  return c->release_slots(first, end);
+}
 void context_upload(Context* c, uint64_t slot, uint64_t count, const uint32_t* lwe) {
   c->upload(slot, count, lwe);
 }
 void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe) {
   c->download(slot, count, lwe);
+}
+void context_gather_download(Context* c, const uint64_t* slots, uint64_t count,
+                             uint32_t* lwe) {
+  c->gather_download(slots, count, lwe);
 }
 void context_submit_level(Context* c, const cvm_gate* g, uint64_t n) { c->submit_level(g, n); }
 void context_sync(Context* c) { c->sync(); }

@@ -62,9 +62,13 @@ void context_upload_keys(Context* c, const uint32_t* bk, const uint32_t* ksk);
 void context_reserve(Context* c, uint64_t n);
 uint64_t context_alloc_slots(Context* c, uint64_t n);  // returns first slot id
 uint64_t context_slots_used(const Context* c);
+bool context_release_slots(Context* c, uint64_t first, uint64_t end);
 uint64_t context_capacity(const Context* c);
 void context_upload(Context* c, uint64_t slot, uint64_t count, const uint32_t* lwe);
 void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe);
+// Any slot list -> one contiguous [count][631] host block (device gather).
+void context_gather_download(Context* c, const uint64_t* slots, uint64_t count,
+                             uint32_t* lwe);
 void context_submit_level(Context* c, const cvm_gate* gates, uint64_t count);
 void context_sync(Context* c);
 Plan* context_make_plan(Context* c, const std::vector<std::vector<cvm_gate>>& levels);
@@ -152,7 +156,12 @@ class GpuBackend final : public Backend {
 
   void decrypt_bits(size_t n, const Bit* hs, uint8_t* out);
   void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
+  void import_lwe_direct(size_t n, const uint32_t* lwe, Bit* out);
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
+  // Give every slot this backend took back to the context if they are the
+  // allocator's top run (call only after the work is synchronised and the
+  // backend will not be used again).  Returns whether they were released.
+  bool release_slots();
   void flush();                             // everything pending
   void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only
   // Flush policy of decrypt/export: the requested cone only (default) or
@@ -181,6 +190,7 @@ class GpuBackend final : public Backend {
   uint64_t enc_counter_ = 0;
   std::vector<Node> nodes_;          // nodes_[id - 1]
   uint64_t next_slot_ = 0, chunk_end_ = 0, chunk_ = 4096;  // slot chunk from ctx
+  std::vector<std::pair<uint64_t, uint64_t>> runs_;  // slot runs taken [first, end)
   // pending uploads (fresh encryptions / imports) and recorded gates
   std::vector<uint32_t> pending_upload_;
   uint64_t pending_upload_slot_ = 0;

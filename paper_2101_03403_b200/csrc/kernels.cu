@@ -13,7 +13,9 @@
 //        wide one bootstrap on 384 threads, the six gadget rows transformed
 //             concurrently (latency default for narrow levels).
 //   key_switch_kernel*      K3+K4: (MUX combine) + LWE key switch N=1024 -> 630;
-//                               one CTA per gate, or 6 position groups per gate.
+//                               one CTA per gate, or 6 position groups per gate,
+//                               or a whole level as one INT8 tensor-core product
+//                               (key_switch_mma_kernel, wide levels).
 //
 // All variants produce bit-identical ciphertexts (tests/test_gpu_parity.py).
 // DESIGN.md section 4 gives the roofline of each kernel; measured variant
@@ -722,6 +724,209 @@ __global__ void __launch_bounds__(kKsWideThreads) key_switch_wide_kernel(
 }
 
 // ------------------------------------------------- FP64 pipe peak probe --
+// ------------------------------------------- K3 + K4 on the tensor cores --
+// The key switch of a whole level as one integer matrix product:
+//   out[g][col] = b_g - sum_{i,j} KSK[i][j][d_gij][col]
+//              = b_g - (A x B)[g][col],  A[g][(i,j,v)] = [d_gij == v] (one-hot),
+// B[(i,j,v)][col] = KSK[i][j][v][col].  B's 32-bit torus words are split into
+// four byte limbs, each multiplied exactly on the INT8 tensor cores (mma.sync
+// m16n8k32 u8 x u8 -> s32: a column sum is at most 8192 * 255 < 2^31) and
+// recombined mod 2^32 as sum_l acc_l << 8l -- bit-identical to the gathers.
+// K = 1024 coefficients x 8 digits x 4 values (the v = 0 rows are zero), one
+// coefficient per k32 step: A's byte k = 4j + v of a step is the one-hot of
+// digit j, so a thread's A register is just 1 << 8*digit.
+//
+// CTA tile: 128 gates x 48 columns x 4 limbs; 8 warps = 4 gate groups (32
+// gates = 2 m16 tiles) x 2 column groups (24 columns = 3 n8 tiles); every B
+// fragment feeds both m tiles.  B chunks (4 coefficients, 48 KB... 57 KB with
+// padding) and the gates' digit words stream through a 2-stage cp.async ring.
+//
+// B layout in HBM (kskb, built once per key upload by ksk_to_limbs_kernel):
+//   [i 1024][limb 4][j 8][col 632] u32 = bytes v = 0..3 of limb l of
+//   KSK[i][j][v][col]   (82.8 MB).
+constexpr int kKsmGates = 128;
+constexpr int kKsmCols = 48;
+constexpr int kKsmColTiles = (kKskRowStride + kKsmCols - 1) / kKsmCols;  // 14
+constexpr int kKsmChunk = 4;                                             // coefficients / stage
+constexpr int kKsmBStride = 56;  // padded column stride: conflict-free fragment loads
+constexpr int kKsmThreads = 256;
+
+struct KsmSmem {
+  uint32_t b[2][kKsmChunk][4][8][kKsmBStride];
+  uint32_t abar[2][kKsmChunk][kKsmGates];
+  KsJob job[kKsmGates];
+  uint32_t bval[kKsmGates];
+};
+
+__global__ void __launch_bounds__(256) ksk_to_limbs_kernel(const uint32_t* __restrict__ ksk,
+                                                           uint32_t* __restrict__ kskb) {
+  // one thread per (i, l, j, col) output word
+  const size_t idx = size_t(blockIdx.x) * 256 + threadIdx.x;
+  const size_t total = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
+  if (idx >= total) return;
+  const int col = int(idx % kKskRowStride);
+  const int j = int((idx / kKskRowStride) % kKsT);
+  const int l = int((idx / (size_t(kKskRowStride) * kKsT)) % 4);
+  const int i = int(idx / (size_t(kKskRowStride) * kKsT * 4));
+  uint32_t w = 0;
+#pragma unroll
+  for (int v = 0; v < kKsBase; ++v) {
+    const uint32_t x = ksk[((size_t(i) * kKsT + j) * kKsBase + v) * kKskRowStride + col];
+    w |= ((x >> (8 * l)) & 0xFFu) << (8 * v);
+  }
+  kskb[idx] = w;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                       uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(kKsmThreads) key_switch_mma_kernel(
+    const KsJob* __restrict__ jobs, int count, const uint32_t* __restrict__ xlwe,
+    const uint32_t* __restrict__ kskb, uint32_t* __restrict__ slab) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  KsmSmem& sm = *reinterpret_cast<KsmSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g0 = blockIdx.x * kKsmGates;
+  const int c0 = blockIdx.y * kKsmCols;
+  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
+
+  if (tid < kKsmGates) {
+    const int g = g0 + tid;
+    KsJob jb = jobs[g < count ? g : 0];
+    sm.job[tid] = jb;
+    uint32_t b = xlwe[size_t(jb.x[0]) * kXlweStride + kPolyN] + jb.cst;
+    if (jb.x[1] != kNoInput) b += xlwe[size_t(jb.x[1]) * kXlweStride + kPolyN];
+    sm.bval[tid] = b;
+  }
+  __syncthreads();
+
+  // stage loaders: B rows (i, l, j) of 48 columns as 12 x 16 B; digit words
+  // abar[i][g] = x0 + x1 + prec for the chunk's 4 coefficients (one uint4 per
+  // gate and input)
+  auto load_b = [&](int stage, int chunk) {
+    for (int e = tid; e < kKsmChunk * 4 * 8 * 12; e += kKsmThreads) {
+      const int seg = e % 12, row = e / 12;  // row = (ii*4 + l)*8 + j
+      const int col = c0 + seg * 4;
+      if (col >= kKskRowStride) continue;
+      const int ii = row / 32, lj = row % 32;
+      const uint32_t* src = kskb + (size_t(chunk * kKsmChunk + ii) * 32 + lj) * kKskRowStride + col;
+      cp_async16(&sm.b[stage][ii][lj >> 3][lj & 7][seg * 4], src);
+    }
+  };
+  auto load_abar = [&](int chunk, uint4& v) {
+    if (tid < kKsmGates) {
+      const KsJob& jb = sm.job[tid];
+      v = *reinterpret_cast<const uint4*>(xlwe + size_t(jb.x[0]) * kXlweStride +
+                                          chunk * kKsmChunk);
+      if (jb.x[1] != kNoInput) {
+        const uint4 w = *reinterpret_cast<const uint4*>(
+            xlwe + size_t(jb.x[1]) * kXlweStride + chunk * kKsmChunk);
+        v.x += w.x;
+        v.y += w.y;
+        v.z += w.z;
+        v.w += w.w;
+      }
+    }
+  };
+  auto store_abar = [&](int stage, const uint4& v) {
+    if (tid < kKsmGates) {
+      sm.abar[stage][0][tid] = v.x + prec;
+      sm.abar[stage][1][tid] = v.y + prec;
+      sm.abar[stage][2][tid] = v.z + prec;
+      sm.abar[stage][3][tid] = v.w + prec;
+    }
+  };
+
+  const int wg = warp & 3, wc = warp >> 2;
+  const int grp = lane >> 2, tig = lane & 3;
+  int acc[2][3][4][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[mt][nt][l][r] = 0;
+
+  constexpr int kChunks = kPolyN / kKsmChunk;  // 256
+  uint4 xv = {0, 0, 0, 0};
+  load_b(0, 0);
+  cp_async_commit();
+  load_abar(0, xv);
+  store_abar(0, xv);
+  for (int c = 0; c < kChunks; ++c) {
+    const int st = c & 1;
+    cp_async_wait_all();
+    __syncthreads();  // chunk c resident; everyone is done with stage st ^ 1
+    if (c + 1 < kChunks) {
+      load_b(st ^ 1, c + 1);
+      cp_async_commit();
+      load_abar(c + 1, xv);
+    }
+#pragma unroll
+    for (int ii = 0; ii < kKsmChunk; ++ii) {
+      uint32_t a[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int gl = wg * 32 + mt * 16 + grp;
+        const uint32_t lo = sm.abar[st][ii][gl], hi = sm.abar[st][ii][gl + 8];
+        const int s0 = 30 - 2 * tig, s1 = 22 - 2 * tig;  // digits tig and tig + 4
+        a[mt][0] = 1u << (8 * ((lo >> s0) & 3u));
+        a[mt][1] = 1u << (8 * ((hi >> s0) & 3u));
+        a[mt][2] = 1u << (8 * ((lo >> s1) & 3u));
+        a[mt][3] = 1u << (8 * ((hi >> s1) & 3u));
+      }
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        const int col = wc * 24 + nt * 8 + grp;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          const uint32_t b0 = sm.b[st][ii][l][tig][col];
+          const uint32_t b1 = sm.b[st][ii][l][tig + 4][col];
+          mma_u8(acc[0][nt][l], a[0], b0, b1);
+          mma_u8(acc[1][nt][l], a[1], b0, b1);
+        }
+      }
+    }
+    if (c + 1 < kChunks) store_abar(st ^ 1, xv);
+  }
+
+  // epilogue: recombine the limbs, subtract from b (column 630), write
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int gl = wg * 32 + mt * 16 + grp + (r >= 2 ? 8 : 0);
+        const int col = c0 + wc * 24 + nt * 8 + tig * 2 + (r & 1);
+        if (g0 + gl >= count || col >= kKskRowStride) continue;
+        const uint32_t sum = uint32_t(acc[mt][nt][0][r]) + (uint32_t(acc[mt][nt][1][r]) << 8) +
+                             (uint32_t(acc[mt][nt][2][r]) << 16) +
+                             (uint32_t(acc[mt][nt][3][r]) << 24);
+        const uint32_t base = col == kN ? sm.bval[gl] : 0u;
+        slab[size_t(sm.job[gl].out_slot) * kLweStride + col] = base - sum;
+      }
+}
+
 // The roofline denominator for the FFT kernel: MEASURED_PEAKS.json carries
 // only HBM and bf16 figures, so the DFMA peak is measured live (8 independent
 // FMA chains per thread, 148 x 8 CTAs of 256 threads).
@@ -740,7 +945,28 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters) 
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// Result download: slab rows (stride 632) of an arbitrary slot list packed
+// into [count][631] for one D2H copy.
+__global__ void __launch_bounds__(256) gather_lwe_kernel(const uint32_t* __restrict__ slab,
+                                                         const uint64_t* __restrict__ slots,
+                                                         uint64_t count,
+                                                         uint32_t* __restrict__ out) {
+  const uint64_t total = count * kLweWords;
+  for (uint64_t e = uint64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
+       e += uint64_t(gridDim.x) * 256) {
+    const uint64_t r = e / kLweWords, w = e - r * kLweWords;
+    out[e] = slab[slots[r] * kLweStride + w];
+  }
+}
+
 // ----------------------------------------------------------- launchers --
+cudaError_t launch_gather_lwe(const uint32_t* slab, const uint64_t* slots, uint64_t count,
+                              uint32_t* out, cudaStream_t s) {
+  const uint64_t total = count * kLweWords;
+  const unsigned blocks = unsigned(std::min<uint64_t>((total + 255) / 256, 148 * 16));
+  gather_lwe_kernel<<<blocks, 256, 0, s>>>(slab, slots, count, out);
+  return cudaGetLastError();
+}
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s) {
   fp64_peak_kernel<<<blocks, 256, 0, s>>>(out, iters);
   return cudaGetLastError();
@@ -817,7 +1043,7 @@ int ks_variant() {
   return g_ks_variant;
 }
 void set_ks_variant(int v) { g_ks_variant = v; }
-bool valid_ks_variant(int v) { return v == 0 || v == 1 || v == 6; }
+bool valid_ks_variant(int v) { return v == 0 || v == 1 || v == 6 || v == 7; }
 
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
@@ -859,20 +1085,37 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   }
 }
 
+cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s) {
+  const size_t total = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
+  ksk_to_limbs_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(ksk, kskb);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
-                              const uint32_t* ksk, uint32_t* slab, cudaStream_t s) {
+                              const uint32_t* ksk, const uint32_t* kskb, uint32_t* slab,
+                              cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
   int variant = ks_variant();
-  // auto: the 6-group kernel is 10x faster on narrow levels; with the zero
-  // digit rows skipped the 1-group kernel is ~8% faster on wide ones
+  // auto: the 6-group gather kernel on narrow levels (10x faster than one
+  // gate per CTA), the tensor-core product on wide ones
   // (profiles/r01_variant_sweep.txt)
-  if (variant == 0) variant = count >= 1024 ? 1 : 6;
+  if (variant == 0) variant = count >= kKsMmaMinGates ? 7 : 6;
   switch (variant) {
     case 1: key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab); break;
     case 6:
       key_switch_wide_kernel<<<count, kKsWideThreads, 0, s>>>(jobs, xlwe, k4, slab);
       break;
+    case 7: {
+      if (!kskb) return cudaErrorInvalidValue;
+      static bool configured = false;
+      const int smem = int(sizeof(KsmSmem));
+      cudaError_t e = set_smem(key_switch_mma_kernel, smem, configured);
+      if (e != cudaSuccess) return e;
+      const dim3 grid((count + kKsmGates - 1) / kKsmGates, kKsmColTiles);
+      key_switch_mma_kernel<<<grid, kKsmThreads, smem, s>>>(jobs, count, xlwe, kskb, slab);
+      break;
+    }
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -44,13 +44,23 @@ int br_variant();
 void set_br_variant(int v);
 bool valid_br_variant(int v);
 // Key-switch kernel: 1 = one gate per CTA; 6 = one gate per 948-thread CTA
-// (6 position groups, latency); 0 = auto by level width.  Env CVM_KS_KERNEL.
+// (6 position groups, latency); 7 = the whole level as one INT8 tensor-core
+// product (one-hot digits x byte limbs of the KSK); 0 = auto by level width
+// (6 below kKsMmaMinGates gates, else 7).  Env CVM_KS_KERNEL.
 constexpr int kDefaultKsVariant = 0;
+constexpr int kKsMmaMinGates = 768;
 int ks_variant();
 void set_ks_variant(int v);
 bool valid_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
+cudaError_t launch_gather_lwe(const uint32_t* slab, const uint64_t* slots, uint64_t count,
+                              uint32_t* out, cudaStream_t s);
+// kskb: the KSK as byte limbs for variant 7 (see kernels.cu), built by
+// launch_ksk_to_limbs from the padded [i][j][v][632] KSK.
+cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s);
+constexpr size_t kKskbWords = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
-                              const uint32_t* ksk, uint32_t* slab, cudaStream_t s);
+                              const uint32_t* ksk, const uint32_t* kskb, uint32_t* slab,
+                              cudaStream_t s);
 
 }  // namespace cvm

@@ -73,7 +73,7 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
-@pytest.mark.parametrize("ks_variant", [1, 6])
+@pytest.mark.parametrize("ks_variant", [1, 6, 7])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
     (two extracted samples + 1/8) and a partially filled last CTA."""
@@ -181,3 +181,34 @@ def test_fu_batch_add16_decrypts(keyset, ctx):
     assert np.array_equal(vals, (av + bv) % (1 << 17))
     assert st["last_flush_levels"] == 9
     assert st["bootstrapped"] == 195 * batch
+
+
+def test_key_switch_tensor_core_multi_tile(keyset, ctx):
+    """The INT8 tensor-core key switch (variant 7) over several 128-gate tiles
+    with a partial last tile, MUX and binary gates mixed: bit-identical to the
+    gather kernel (variant 6, itself pinned to the oracle above)."""
+    from paper_2101_03403_b200._native import lib, check
+    n = 300
+    s, t, f = _bits(n, 18), _bits(n, 19), _bits(n, 20)
+    cs, ct, cf = keyset.encrypt(s, 71), keyset.encrypt(t, 72), keyset.encrypt(f, 73)
+    base = ctx.alloc(5 * n)
+    for k, c in enumerate((cs, ct, cf)):
+        ctx.upload(base + k * n, c)
+    gates = [("MUX", [(base + i, 1, 0), (base + n + i, 1, 0), (base + 2 * n + i, 1, 0)],
+              base + 3 * n + i) for i in range(n)]
+    gates += [("XNOR", [(base + i, 1, 0), (base + n + i, 1, 0)], base + 4 * n + i)
+              for i in range(n)]
+    outs = {}
+    old = lib.cvm_get_ks_variant()
+    try:
+        for v in (6, 7):
+            check(lib.cvm_set_ks_variant(v))
+            ctx.submit_level(gates)
+            ctx.sync()
+            outs[v] = ctx.download(base + 3 * n, 2 * n)
+    finally:
+        check(lib.cvm_set_ks_variant(old))
+    assert np.array_equal(outs[6], outs[7])
+    bits = keyset.decrypt(outs[7])
+    assert np.array_equal(bits[:n], np.where(s == 1, t, f))
+    assert np.array_equal(bits[n:], 1 - (s ^ t))
