@@ -397,7 +397,57 @@ struct BrSmem3 {
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
   uint64_t full[S], empty[S];
+  uint64_t tfull[S], tempty[S];  // TMEM key ring (kTmem)
+  uint32_t tmem_base;
 };
+
+// ---- tcgen05 / TMEM helpers (v3 with the key ring in tensor memory) ----
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Shared-memory matrix descriptor of a [rows][16 B] block, no swizzle: core
+// matrices of 8 rows x 16 B are contiguous (128 B apart in both directions).
+__device__ __forceinline__ uint64_t smem_desc_rows16(const void* p) {
+  const uint64_t a = smem_u32(p);
+  return ((a >> 4) & 0x3FFFull) | (uint64_t(128 >> 4) << 16) | (uint64_t(128 >> 4) << 32) |
+         (1ull << 46);
+}
+// 64 rows x 128 bit smem -> TMEM, rows 0-31 to lane quarters 0 and 2, rows
+// 32-63 to quarters 1 and 3: thread t of every bootstrap finds its value in
+// its own lane whichever warp pair the bootstrap runs on.
+__device__ __forceinline__ void tc_cp_64x128_0213(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.64x128b.warpx2::02_13 [%0], %1;" ::"r"(taddr), "l"(desc)
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// 8 consecutive 32-bit columns of this thread's lane (= two complex doubles).
+// The registers are written asynchronously: read them only after
+// tc_wait_ld16, which takes them as operands so no use is hoisted above it.
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld16(uint32_t (&a)[8], uint32_t (&b)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]),
+                 "+r"(a[6]), "+r"(a[7]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]),
+                 "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
+               :
+               : "memory");
+}
+__device__ __forceinline__ c64 c64_of(const uint32_t* r) {
+  return {__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2])};
+}
 
 // chunk q (0 .. 6n-1, pair order) -> TRGSW row in the FFT-domain key
 __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
@@ -406,12 +456,19 @@ __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
   return bkf + ((size_t)i * kRows + row) * 1024;
 }
 
-template <int G, int S>
+// kTmem: the key rows are copied once per CTA from the shared-memory ring
+// into a tensor-memory ring (tcgen05.cp, 64 columns per row, each thread's
+// bins in its own lane) and every bootstrap reads them with tcgen05.ld --
+// the G-fold shared-memory key reads leave the LSU path.  Thread 0 stages:
+// TMA row c -> smem slot c%4 -> (after the consumers released TMEM slot c%4)
+// tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
+template <int G, int S, bool kTmem = false>
 __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
   static_assert(S >= 4, "pairs need two chunks in flight plus prefetch");
+  static_assert(!kTmem || S == 4, "the TMEM ring mirrors a 4-slot smem ring");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BrSmem3<G, S>& sm = *reinterpret_cast<BrSmem3<G, S>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -421,19 +478,54 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
   const bool live = jidx < count;
   const BrJob job = jobs[live ? jidx : 0];
   constexpr int kChunks = kN * kRows;
+  constexpr uint32_t kTmemCols = 64 * 4;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 64 * G);
+      mbar_init(&sm.tfull[s], 1);
+      mbar_init(&sm.tempty[s], 64 * G);
     }
     mbar_init_fence();
   }
+  if constexpr (kTmem) {
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&sm.tmem_base)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+  }
   __syncthreads();
+  uint32_t tbase = 0, tlane = 0;
+  if constexpr (kTmem) {
+    tc_fence_after();
+    tbase = sm.tmem_base;
+    tlane = uint32_t(32 * ((tid >> 5) & 3)) << 16;  // this warp's lane quarter
+  }
+  // thread 0: copy staged row c (smem slot c%4) into TMEM slot c%4
+  auto stage_tmem = [&](int c) {
+    const int s = c & 3;
+    if (c >= 4) mbar_wait(&sm.tempty[s], ((c - 4) >> 2) & 1);
+    mbar_wait(&sm.full[s], (c >> 2) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int blk = 0; blk < 16; ++blk)
+      tc_cp_64x128_0213(tbase + uint32_t(s * 64 + blk * 4),
+                        smem_desc_rows16(&sm.ring[s][blk * 64]));
+    tc_commit(&sm.tfull[s]);
+  };
   if (tid == 0) {
     for (int q = 0; q < S; ++q) {
       mbar_expect_tx(&sm.full[q], kRowBytes);
       bulk_g2s(sm.ring[q], chunk_src(bkf, q), kRowBytes, &sm.full[q]);
+    }
+    if constexpr (kTmem) {
+      stage_tmem(0);
+      stage_tmem(1);
     }
   }
   c64 T1[8], T2[8];
@@ -483,31 +575,64 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
       exchange_pair<2>(va, vb, xa, xb, t, bar_id);
       fwd_stage3(va);
       fwd_stage3(vb);
-      // producer: refill the slots of chunks q-2, q-1 with chunks q+S-2, q+S-1
-      if (tid == 0) {
+      const int sa = q % S, sb = (q + 1) % S;
+      if constexpr (!kTmem) {
+        // producer: refill the slots of chunks q-2, q-1 with chunks q+S-2, q+S-1
+        if (tid == 0) {
 #pragma unroll
-        for (int c = q - 2; c < q; ++c) {
-          if (c < 0 || c + S >= kChunks) continue;
-          const int slot = c % S;
-          mbar_wait(&sm.empty[slot], (c / S) & 1);
-          mbar_expect_tx(&sm.full[slot], kRowBytes);
-          bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+          for (int c = q - 2; c < q; ++c) {
+            if (c < 0 || c + S >= kChunks) continue;
+            const int slot = c % S;
+            mbar_wait(&sm.empty[slot], (c / S) & 1);
+            mbar_expect_tx(&sm.full[slot], kRowBytes);
+            bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+          }
+        }
+        mbar_wait(&sm.full[sa], (q / S) & 1);
+        mbar_wait(&sm.full[sb], ((q + 1) / S) & 1);
+        const c64* bka = sm.ring[sa];
+        const c64* bkb = sm.ring[sb];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
+          const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
+          af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
+          af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
+        }
+        mbar_arrive(&sm.empty[sa]);
+        mbar_arrive(&sm.empty[sb]);
+      } else {
+        mbar_wait(&sm.tfull[sa], (q >> 2) & 1);
+        mbar_wait(&sm.tfull[sb], ((q + 1) >> 2) & 1);
+        tc_fence_after();
+        const uint32_t ta = tbase + tlane + uint32_t(sa * 64);
+        const uint32_t tb = tbase + tlane + uint32_t(sb * 64);
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          uint32_t ra[8], rb[8];
+          tc_ld8(ta + uint32_t(k2 * 8), ra);  // (k2, o = 0, 1) of row a
+          tc_ld8(tb + uint32_t(k2 * 8), rb);
+          tc_wait_ld16(ra, rb);
+          af[0][k2] = cmac(cmac(af[0][k2], va[k2], c64_of(ra)), vb[k2], c64_of(rb));
+          af[1][k2] = cmac(cmac(af[1][k2], va[k2], c64_of(ra + 4)), vb[k2], c64_of(rb + 4));
+        }
+        tc_fence_before();
+        mbar_arrive(&sm.tempty[sa]);
+        mbar_arrive(&sm.tempty[sb]);
+        if (tid == 0) {
+          // smem slots of chunks q, q+1 were read by their (completed) copies:
+          // stream chunks q+4, q+5 into them; then copy chunks q+2, q+3
+          // (staged one pair ago) into TMEM slots freed by chunks q-2, q-1
+#pragma unroll
+          for (int c = q + 4; c < q + 6; ++c) {
+            if (c >= kChunks) continue;
+            mbar_expect_tx(&sm.full[c & 3], kRowBytes);
+            bulk_g2s(sm.ring[c & 3], chunk_src(bkf, c), kRowBytes, &sm.full[c & 3]);
+          }
+          if (q + 2 < kChunks) stage_tmem(q + 2);
+          if (q + 3 < kChunks) stage_tmem(q + 3);
         }
       }
-      const int sa = q % S, sb = (q + 1) % S;
-      mbar_wait(&sm.full[sa], (q / S) & 1);
-      mbar_wait(&sm.full[sb], ((q + 1) / S) & 1);
-      const c64* bka = sm.ring[sa];
-      const c64* bkb = sm.ring[sb];
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) {
-        const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
-        const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
-        af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
-        af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
-      }
-      mbar_arrive(&sm.empty[sa]);
-      mbar_arrive(&sm.empty[sb]);
     }
     inv_stageA(af[0]);
     inv_stageA(af[1]);
@@ -522,6 +647,16 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
   }
   group_sync(bar_id);
   if (live) extract(acc0, acc1, xout + (size_t)job.out * kXlweStride, t, 64);
+  if constexpr (kTmem) {
+    tc_fence_before();
+    __syncthreads();
+    if (tid < 32) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                   "r"(kTmemCols)
+                   : "memory");
+    }
+  }
 }
 
 // ------------------------------------------------ K1 + K2, latency: wide --
@@ -800,7 +935,7 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint
 __global__ void __launch_bounds__(kKsmThreads) key_switch_mma_kernel(
     const KsJob* __restrict__ jobs, int count, const uint32_t* __restrict__ xlwe,
     const uint32_t* __restrict__ kskb, uint32_t* __restrict__ slab) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   KsmSmem& sm = *reinterpret_cast<KsmSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g0 = blockIdx.x * kKsmGates;
@@ -998,15 +1133,15 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S>
+template <int G, int S, bool kTmem = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S>));
-  cudaError_t e = set_smem(blind_rotate_kernel_v3<G, S>, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_kernel_v3<G, S, kTmem>, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_kernel_v3<G, S><<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf,
-                                                                       tw1, tw2, xout);
+  blind_rotate_kernel_v3<G, S, kTmem><<<(count + G - 1) / G, 64 * G, smem, s>>>(
+      jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
@@ -1034,7 +1169,7 @@ int br_variant() {
 void set_br_variant(int v) { g_br_variant = v; }
 int default_br_variant() { return kDefaultBrVariant; }
 bool valid_br_variant(int v) {
-  return v == 0 || v == 1 || v == 9 || v == 13 || v == 22 || v == 23 || v == 43 || v == 3044;
+  return v == 0 || v == 1 || v == 9 || v == 13 || v == 22 || v == 23 || v == 43 || v == 3044 || v == 4044;
 }
 
 static int g_ks_variant = -1;
@@ -1081,6 +1216,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 43: return launch_v2<4, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 4044: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
