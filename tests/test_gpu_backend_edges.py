@@ -1,0 +1,131 @@
+"""Backend contract edge cases on the device path (gates.hpp:109-132 semantics,
+SURVEY §8 a-2, a-5, a-7, a-16): folded free ops at export time, blob round
+trips and the InputError paths, plan replay on new inputs, slab growth,
+scratch-slot reuse by cvm_fu_batch, and concurrent recording."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2101_03403_b200 as P
+from paper_2101_03403_b200._native import CvmInputError, lib
+
+pytestmark = pytest.mark.gpu
+MU = 1 << 29
+
+
+def test_export_folded_constants_negations_and_duplicates(keyset, ctx):
+    bk = P.Backend(ctx, keyset)
+    a = bk.encrypt_bit(1)
+    c0, c1 = bk.constant(False), bk.constant(True)
+    na = bk.unary_gate("NOT", a)
+    cp = bk.unary_gate("COPY", na)
+    g = bk.binary_gate("AND", a, c1)  # a bootstrapped gate with a constant input
+    hs = [c0, c1, na, cp, a, a, g, c0]
+    raw = bk.export_lwe(hs)
+    assert list(keyset.decrypt(raw)) == [0, 1, 0, 0, 1, 1, 1, 0]
+    # trivial samples: a = 0, b = -+1/8
+    assert not raw[0, :630].any() and raw[0, 630] == (0 - MU) % 2**32
+    assert not raw[1, :630].any() and raw[1, 630] == MU
+    # NOT is the negation of every word; COPY aliases it; duplicates agree
+    assert np.array_equal(raw[2], (0 - raw[4].astype(np.int64)) % 2**32)
+    assert np.array_equal(raw[2], raw[3]) and np.array_equal(raw[4], raw[5])
+
+
+def test_blob_round_trip_and_input_errors(keyset, ctx):
+    bk = P.Backend(ctx, keyset)
+    h = bk.binary_gate("XOR", bk.encrypt_bit(1), bk.encrypt_bit(0))
+    blob = bk.export_bit(h)
+    assert len(blob) == 631 * 4
+    h2 = bk.import_bit(blob)
+    assert bk.decrypt_bit(h2) is True
+    assert bk.decrypt_bit(bk.unary_gate("NOT", h2)) is False
+    with pytest.raises(CvmInputError):
+        bk.import_bit(blob[:-1])              # sim_backend.cpp:124-126
+    with pytest.raises(CvmInputError):
+        bk.decrypt_bit(10**9)                  # invalid handle, :53-57
+    with pytest.raises(CvmInputError):
+        bk.binary_gate("NOT", h, h2)           # wrong kind, :47-49
+    with pytest.raises(CvmInputError):
+        bk.unary_gate("AND", h)                # :80-83
+    with pytest.raises(CvmInputError):
+        bk.pop_region()                        # unbalanced, :140-142
+
+
+def test_plan_replay_on_new_inputs(keyset, ctx):
+    """A captured 8-bit adder replays (CUDA graph or plain launches) on new
+    ciphertexts written into its input slots."""
+    rng = np.random.default_rng(5)
+    bk = P.Backend(ctx, keyset)
+    a = bk.import_lwe(keyset.encrypt_words(np.array([0]), 8, 1).reshape(-1, 631))
+    b = bk.import_lwe(keyset.encrypt_words(np.array([0]), 8, 2).reshape(-1, 631))
+    outs = bk.fu("add", a, b)
+    plan = bk.capture_plan()
+    assert plan.info()["gates"] > 0
+    slots_a = [bk.handle_slot(h)[0] for h in a]
+    slots_b = [bk.handle_slot(h)[0] for h in b]
+    for trial, graph in enumerate((True, False, True)):
+        x, y = (int(v) for v in rng.integers(0, 256, 2))
+        ca = keyset.encrypt_words(np.array([x]), 8, 10 + trial).reshape(-1, 631)
+        cb = keyset.encrypt_words(np.array([y]), 8, 20 + trial).reshape(-1, 631)
+        for i in range(8):
+            ctx.upload(slots_a[i], ca[i])
+            ctx.upload(slots_b[i], cb[i])
+        plan.run(ctx, graph=graph)
+        ctx.sync()
+        got = keyset.decrypt_words(bk.export_lwe(outs), 9)[0]
+        assert got == x + y, (trial, graph)
+
+
+def test_submit_level_rejects_bad_levels(ctx):
+    n = ctx.alloc(2)
+    with pytest.raises(CvmInputError):  # NOT is not a bootstrapped kind
+        ctx.submit_level([("NOT", [(n, 1, 0)], n + 1)])
+    with pytest.raises(CvmInputError):  # output slot beyond capacity
+        ctx.submit_level([("AND", [(n, 1, 0), (n, 1, 0)], 1 << 40)])
+
+
+def test_slab_growth_preserves_contents(keyset, ctx):
+    bits = np.array([1, 0, 1, 1, 0], np.uint8)
+    c = keyset.encrypt(bits, 77)
+    first = ctx.alloc(len(bits))
+    ctx.upload(first, c)
+    cap0 = lib.cvm_slots_capacity(ctx.handle)
+    ctx.alloc(cap0 + 50_000)  # forces a reallocation of the slab
+    assert lib.cvm_slots_capacity(ctx.handle) > cap0
+    assert np.array_equal(ctx.download(first, len(bits)), c)
+
+
+def test_fu_batch_reuses_its_scratch_slots(keyset, ctx):
+    a = keyset.encrypt_words(np.arange(32) * 7 % 65536, 16, 3)
+    b = keyset.encrypt_words(np.arange(32) * 13 % 65536, 16, 4)
+    P.fu_batch(ctx, "add", 16, a, b)
+    used = lib.cvm_slots_capacity(ctx.handle)
+    for _ in range(3):
+        out, st = P.fu_batch(ctx, "add", 16, a, b)
+    assert lib.cvm_slots_capacity(ctx.handle) == used
+    sums = keyset.decrypt_words(out.reshape(-1, 631), 17)
+    assert np.array_equal(sums, (np.arange(32) * 7 % 65536) + (np.arange(32) * 13 % 65536))
+
+
+def test_concurrent_recording_threads(keyset, ctx):
+    """gates.hpp:102-104: independent gates may be recorded concurrently."""
+    bk = P.Backend(ctx, keyset)
+    n_threads, per = 4, 12
+    rng = np.random.default_rng(9)
+    xs = rng.integers(0, 2, (n_threads, per, 2))
+    ins = [[(bk.encrypt_bit(int(p[0])), bk.encrypt_bit(int(p[1]))) for p in row] for row in xs]
+    outs = [[None] * per for _ in range(n_threads)]
+
+    def work(k):
+        for i, (ha, hb) in enumerate(ins[k]):
+            outs[k][i] = bk.binary_gate("NAND", bk.binary_gate("XOR", ha, hb), ha)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(n_threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    got = bk.decrypt_bits(np.array(outs, np.uint64).ravel()).reshape(n_threads, per)
+    want = 1 - ((xs[..., 0] ^ xs[..., 1]) & xs[..., 0])
+    assert np.array_equal(got, want)
