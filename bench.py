@@ -126,6 +126,17 @@ def cpu_sample_inputs(sk, n_gates, seed=7):
     return kinds, a, b
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(target_s=12.0, threads=None):
     """Oracle (double-FFT TFHE, the library's method) on all host threads."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
@@ -145,7 +156,8 @@ def cpu_baseline(target_s=12.0, threads=None):
     dt = time.perf_counter() - t
     dec = sk.decrypt(out)
     return {"value": n / dt, "unit": "bootstrapped gates/s", "cores": threads,
-            "kind": "port", "seconds": dt,
+            "kind": "port", "seconds": dt, "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
             "sample": f"{n} AND/XOR gates of the ADD16 batch's first dataflow level, "
                       f"oracle/ double-FFT TFHE (the TFHE library's method), {threads} threads",
             "decrypt_sanity": int(dec.size)}
@@ -180,7 +192,7 @@ def run_reference(args):
                    "sample_per_step": f"{n} gates of the first dataflow level",
                    "parallelism": f"cpu threads={threads}"},
         "cpu_baseline": {"value": value, "unit": "bootstrapped gates/s", "cores": threads,
-                         "kind": "port",
+                         "kind": "port", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{n} AND/XOR gates per step, double-FFT TFHE (oracle/)"},
         "e2e": {"value": value, "unit": "bootstrapped gates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
