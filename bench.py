@@ -211,6 +211,10 @@ def extra_configs(P, ctx, ks):
     import json as _json
     rng = np.random.default_rng(77)
     out = {}
+    # cvm_fu_batch returns its scratch slots, so the slab only holds the
+    # largest single call; size it once for config 4 (216k gates + inputs)
+    # instead of growing it by doubling inside a timed call.
+    ctx.reserve(ctx.alloc(0) + 300_000)
 
     def fu(op, batch, seed):
         av = rng.integers(0, 1 << WIDTH, batch)

@@ -144,9 +144,11 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * the key read through L1; 10*G+S = G bootstraps per CTA sharing an S-stage
  * bulk-copy shared-memory key ring (13, 22, 23, 43); 3044 = four bootstraps
  * per CTA, two transforms in flight per thread; 4044 = 3044 with the key
- * ring in tensor memory (tcgen05.cp / tcgen05.ld); 9 = one bootstrap on 384
+ * ring in tensor memory (tcgen05.cp / tcgen05.ld); 5044 / 5054 / 5063 =
+ * 3044 (G=4, 5) / v2 G=6 with per-thread twiddles generated on use (12
+ * resident registers instead of 64); 9 = one bootstrap on 384
  * threads (six gadget rows concurrently, latency).  0 = auto (default): 9 for
- * levels up to 148 bootstraps, 13 up to 296, else 3044.  Every variant
+ * levels up to 148 bootstraps, 13 up to 296, else 5044.  Every variant
  * computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);

@@ -178,6 +178,38 @@ inline void make_twiddles(c64 T1[64][8], c64 T2[64][8]) {
     }
 }
 
+// Per-thread twiddles generated on use, T[k] = base * w^k (k = 0..7), from
+// two resident complex values instead of eight: 9 (or 6 with base 1)
+// complex multiplies per use, a few ulp -- inside the FFT's rounding margin
+// (tests/native/fft_emul.cpp measures both modes), and
+// 52 fewer live registers per thread.  Bases: T1 = (w^t, W_512^t),
+// T2 = W_512^(8 (t>>3)).
+struct TwPow8 {
+  c64 v[8];
+  CVM_HD TwPow8(c64 base, c64 w) {
+    const c64 w2 = cmul(w, w), w4 = cmul(w2, w2);
+    v[0] = base;
+    v[1] = cmul(base, w);
+    v[2] = cmul(base, w2);
+    v[3] = cmul(v[2], w);
+    v[4] = cmul(base, w4);
+    v[5] = cmul(v[4], w);
+    v[6] = cmul(v[4], w2);
+    v[7] = cmul(v[6], w);
+  }
+  CVM_HD explicit TwPow8(c64 w) {  // base 1
+    v[0] = {1.0, 0.0};
+    v[1] = w;
+    v[2] = cmul(w, w);
+    v[3] = cmul(v[2], w);
+    v[4] = cmul(v[2], v[2]);
+    v[5] = cmul(v[4], w);
+    v[6] = cmul(v[4], v[2]);
+    v[7] = cmul(v[6], w);
+  }
+  CVM_HD const c64& operator[](int k) const { return v[k]; }
+};
+
 // ---------------------------------------------------- exact conversions --
 // Small non-negative integer u (< 2^31) to double, exactly, without I2F:
 // the bit pattern 0x43300000:u is the double 2^52 + u.

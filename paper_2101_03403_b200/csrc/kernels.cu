@@ -294,8 +294,24 @@ struct BrSmem2 {
   uint64_t full[S], empty[S];
 };
 
-template <int G, int S>
-__global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
+// Resident bases of the generated twiddles (kTwRec): T1[k] = t1b * t1w^k,
+// T2[k] = t2w^k (see TwPow8).
+struct TwBases {
+  c64 t1b, t1w, t2w;
+};
+__device__ __forceinline__ TwBases tw_bases(const c64* tw1, int t) {
+  TwBases b;
+  b.t1b = ldg_c64(tw1 + t * 8);  // w^t (the fold twist), exact table value
+  double s, c;
+  sincospi(-double(t) / 256.0, &s, &c);  // W_512^t
+  b.t1w = {c, s};
+  sincospi(-double(t >> 3) / 32.0, &s, &c);  // W_512^(8 (t>>3))
+  b.t2w = {c, s};
+  return b;
+}
+
+template <int G, int S, bool kTwRec = false>
+__global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v2(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
@@ -323,8 +339,10 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
       bulk_g2s(sm.ring[q], bkf + (size_t)q * 1024, kRowBytes, &sm.full[q]);
     }
   }
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
+  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
+  TwBases tb{};
+  if constexpr (kTwRec) tb = tw_bases(tw1, t);
+  else load_twiddles(tw1, tw2, t, T1, T2);
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
   uint16_t* bar = sm.bar[g];
@@ -346,9 +364,11 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
       for (int p = 0; p < kL; ++p, ++q) {
         c64 v[8];
         digits(dif, 32 - (p + 1) * kBgBit, v);
-        fwd_stage1(v, T1);
+        if constexpr (kTwRec) fwd_stage1(v, TwPow8(tb.t1b, tb.t1w));
+        else fwd_stage1(v, T1);
         exchange<1>(v, sm.xbuf[g][0], t, sync);
-        fwd_stage2(v, T2);
+        if constexpr (kTwRec) fwd_stage2(v, TwPow8(tb.t2w));
+        else fwd_stage2(v, T2);
         exchange<2>(v, sm.xbuf[g][1], t, sync);
         fwd_stage3(v);
         // producer: refill the slot chunk q-1 used with chunk q+S-1
@@ -373,9 +393,11 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v2(
     for (int o = 0; o < 2; ++o) {
       inv_stageA(af[o]);
       exchange<2>(af[o], sm.xbuf[g][0], t, sync);
-      inv_stageB(af[o], T2);
+      if constexpr (kTwRec) inv_stageB(af[o], TwPow8(tb.t2w));
+      else inv_stageB(af[o], T2);
       exchange<3>(af[o], sm.xbuf[g][1], t, sync);
-      inv_stageC(af[o], T1);
+      if constexpr (kTwRec) inv_stageC(af[o], TwPow8(tb.t1b, tb.t1w));
+      else inv_stageC(af[o], T1);
       add_rounded(o ? acc1 : acc0, af[o], t);
     }
   }
@@ -462,8 +484,10 @@ __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
 // the G-fold shared-memory key reads leave the LSU path.  Thread 0 stages:
 // TMA row c -> smem slot c%4 -> (after the consumers released TMEM slot c%4)
 // tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
-template <int G, int S, bool kTmem = false>
-__global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
+// kTwRec: twiddles generated on use (TwPow8) -- 12 resident registers
+// instead of 64, so five bootstraps (10 warps) fit an SM's register file.
+template <int G, int S, bool kTmem = false, bool kTwRec = false>
+__global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
@@ -528,8 +552,16 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
       stage_tmem(1);
     }
   }
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
+  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
+  c64 t1b{}, t1w{}, t2w{};  // kTwRec: T1[k] = t1b * t1w^k, T2[k] = t2w^k
+  if constexpr (!kTwRec) {
+    load_twiddles(tw1, tw2, t, T1, T2);
+  } else {
+    const TwBases b = tw_bases(tw1, t);
+    t1b = b.t1b;
+    t1w = b.t1w;
+    t2w = b.t2w;
+  }
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
   uint16_t* bar = sm.bar[g];
@@ -567,11 +599,23 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
         vb[x] = {u32_biased_to_double((db0 >> shift) & 127u, kDigitBias),
                  u32_biased_to_double((db1 >> shift) & 127u, kDigitBias)};
       }
-      fwd_stage1(va, T1);
-      fwd_stage1(vb, T1);
+      if constexpr (kTwRec) {
+        const TwPow8 w1(t1b, t1w);
+        fwd_stage1(va, w1);
+        fwd_stage1(vb, w1);
+      } else {
+        fwd_stage1(va, T1);
+        fwd_stage1(vb, T1);
+      }
       exchange_pair<1>(va, vb, xa, xb, t, bar_id);
-      fwd_stage2(va, T2);
-      fwd_stage2(vb, T2);
+      if constexpr (kTwRec) {
+        const TwPow8 w2(t2w);
+        fwd_stage2(va, w2);
+        fwd_stage2(vb, w2);
+      } else {
+        fwd_stage2(va, T2);
+        fwd_stage2(vb, T2);
+      }
       exchange_pair<2>(va, vb, xa, xb, t, bar_id);
       fwd_stage3(va);
       fwd_stage3(vb);
@@ -637,11 +681,23 @@ __global__ void __launch_bounds__(64 * G) blind_rotate_kernel_v3(
     inv_stageA(af[0]);
     inv_stageA(af[1]);
     exchange_pair<2>(af[0], af[1], xa, xb, t, bar_id);
-    inv_stageB(af[0], T2);
-    inv_stageB(af[1], T2);
+    if constexpr (kTwRec) {
+      const TwPow8 w2(t2w);
+      inv_stageB(af[0], w2);
+      inv_stageB(af[1], w2);
+    } else {
+      inv_stageB(af[0], T2);
+      inv_stageB(af[1], T2);
+    }
     exchange_pair<3>(af[0], af[1], xa, xb, t, bar_id);
-    inv_stageC(af[0], T1);
-    inv_stageC(af[1], T1);
+    if constexpr (kTwRec) {
+      const TwPow8 w1(t1b, t1w);
+      inv_stageC(af[0], w1);
+      inv_stageC(af[1], w1);
+    } else {
+      inv_stageC(af[0], T1);
+      inv_stageC(af[1], T1);
+    }
     add_rounded(acc0, af[0], t);
     add_rounded(acc1, af[1], t);
   }
@@ -1121,26 +1177,26 @@ static cudaError_t set_smem(K* kern, int bytes, bool& configured) {
   return e;
 }
 
-template <int G, int S>
+template <int G, int S, bool kTwRec = false>
 static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem2<G, S>));
-  cudaError_t e = set_smem(blind_rotate_kernel_v2<G, S>, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_kernel_v2<G, S, kTwRec>, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_kernel_v2<G, S><<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf,
-                                                                       tw1, tw2, xout);
+  blind_rotate_kernel_v2<G, S, kTwRec><<<(count + G - 1) / G, 64 * G, smem, s>>>(
+      jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTmem = false>
+template <int G, int S, bool kTmem = false, bool kTwRec = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S>));
-  cudaError_t e = set_smem(blind_rotate_kernel_v3<G, S, kTmem>, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_kernel_v3<G, S, kTmem, kTwRec>, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_kernel_v3<G, S, kTmem><<<(count + G - 1) / G, 64 * G, smem, s>>>(
+  blind_rotate_kernel_v3<G, S, kTmem, kTwRec><<<(count + G - 1) / G, 64 * G, smem, s>>>(
       jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
@@ -1169,7 +1225,8 @@ int br_variant() {
 void set_br_variant(int v) { g_br_variant = v; }
 int default_br_variant() { return kDefaultBrVariant; }
 bool valid_br_variant(int v) {
-  return v == 0 || v == 1 || v == 9 || v == 13 || v == 22 || v == 23 || v == 43 || v == 3044 || v == 4044;
+  return v == 0 || v == 1 || v == 9 || v == 13 || v == 22 || v == 23 || v == 43 || v == 3044 || v == 4044 ||
+         v == 5044 || v == 5054 || v == 5063;
 }
 
 static int g_ks_variant = -1;
@@ -1188,9 +1245,10 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   if (variant == 0) {
     // auto: a narrow level runs each bootstrap on a whole SM (latency); a
     // level of up to two bootstraps per SM gives each its own CTA; wide
-    // levels use the throughput kernel, whose SMs work in rounds of 4
-    // bootstraps (~6.6 ms).  A last partial round of at most 2 bootstraps per
-    // SM is cheaper on the latency kernel (2 x 2.3 ms), so it is split off.
+    // levels use the throughput kernel (v3 with generated twiddles, 5044),
+    // whose SMs work in rounds of 4 bootstraps (~6.4 ms).  A last partial
+    // round of at most 2 bootstraps per SM is cheaper on the latency kernel
+    // (2 x 2.3 ms), so it is split off.
     constexpr int kSms = 148, kRound = 4 * kSms;
     if (count <= kSms) {
       variant = 9;
@@ -1199,11 +1257,12 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     } else {
       const int tail = count % kRound;
       if (tail > 0 && tail <= 2 * kSms && count > kRound) {
-        cudaError_t e = launch_v3<4, 4>(jobs, count - tail, slab, bkf, tw1, tw2, xout, s);
+        cudaError_t e =
+            launch_v3<4, 4, false, true>(jobs, count - tail, slab, bkf, tw1, tw2, xout, s);
         if (e != cudaSuccess) return e;
         return launch_wide(jobs + (count - tail), tail, slab, bkf, tw1, tw2, xout, s);
       }
-      variant = 3044;
+      variant = 5044;
     }
   }
   switch (variant) {
@@ -1215,8 +1274,11 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 22: return launch_v2<2, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 43: return launch_v2<4, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5063: return launch_v2<6, 3, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 4044: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5044: return launch_v3<4, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5054: return launch_v3<5, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }

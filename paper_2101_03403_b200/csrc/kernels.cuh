@@ -38,6 +38,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
 // via L1); 10*G + S = v2 (G bootstraps per CTA, S-stage bulk-copy key ring:
 // 13, 22, 23, 43); 3044 = v3 (G=4, S=4, two transforms per thread);
 // 4044 = v3 with the key ring in tensor memory (tcgen05.cp / tcgen05.ld);
+// 5044 / 5054 / 5063 = v3 G=4 / v3 G=5 / v2 G=6 with generated twiddles
+// (TwPow8; 5044 is the wide-level default);
 // 9 = wide latency kernel.  0 = auto by level width (default).  Env
 // CVM_BR_KERNEL overrides the default.
 constexpr int kDefaultBrVariant = 0;

@@ -3,8 +3,14 @@
 // stage functions, exchange-buffer permutations and swizzle with 64 emulated
 // threads and checks products of random (digit, torus32) polynomials against
 // the exact negacyclic product.  Also checks the swizzle is bank-conflict-free.
+// Two twiddle modes: the host tables (make_twiddles) and the generated
+// twiddles of the kTwRec kernels (TwPow8 from two bases per thread) on the
+// digit side; the key side always uses the tables (bk_to_fft_kernel).  The
+// largest distance of an un-rounded output to the nearest integer is printed
+// per mode -- the rounding margin (a flip needs 0.5).
 //
 // Build+run by tests/test_fft_emul.py:  g++ -O2 -std=c++17 -I<csrc> fft_emul.cpp
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -16,19 +22,32 @@
 using namespace cvm;
 
 static c64 T1[64][8], T2[64][8];
+static c64 B1b[64], B1w[64], B2w[64];  // TwPow8 bases per thread
+static bool g_rec = false;             // digit side uses generated twiddles
+
+struct TabTw {
+  const c64* p;
+  const c64& operator[](int k) const { return p[k]; }
+};
 
 // forward: coefficient poly (as doubles) -> bins[t][k2]
-static void forward(const double* p, c64 bins[64][8]) {
+static void forward(const double* p, c64 bins[64][8], bool rec) {
   c64 v[64][8];
   c64 buf[512];
   for (int t = 0; t < 64; ++t)
     for (int a = 0; a < 8; ++a) v[t][a] = {p[t + 64 * a], p[t + 64 * a + 512]};
-  for (int t = 0; t < 64; ++t) fwd_stage1(v[t], T1[t]);
+  for (int t = 0; t < 64; ++t) {
+    if (rec) fwd_stage1(v[t], TwPow8(B1b[t], B1w[t]));
+    else fwd_stage1(v[t], TabTw{T1[t]});
+  }
   for (int t = 0; t < 64; ++t)
     for (int z = 0; z < 8; ++z) buf[xpos(ex1_cell(t, z), t >> 3)] = v[t][z];
   for (int t = 0; t < 64; ++t)
     for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
-  for (int t = 0; t < 64; ++t) fwd_stage2(v[t], T2[t]);
+  for (int t = 0; t < 64; ++t) {
+    if (rec) fwd_stage2(v[t], TwPow8(B2w[t]));
+    else fwd_stage2(v[t], TabTw{T2[t]});
+  }
   for (int t = 0; t < 64; ++t)
     for (int z = 0; z < 8; ++z) buf[xpos(ex2_cell(t, z), t >> 3)] = v[t][z];
   for (int t = 0; t < 64; ++t)
@@ -39,7 +58,7 @@ static void forward(const double* p, c64 bins[64][8]) {
   }
 }
 
-static void inverse(c64 bins[64][8], uint32_t* out) {
+static void inverse(c64 bins[64][8], uint32_t* out, double* worst) {
   c64 v[64][8];
   c64 buf[512];
   for (int t = 0; t < 64; ++t)
@@ -49,14 +68,22 @@ static void inverse(c64 bins[64][8], uint32_t* out) {
     for (int z = 0; z < 8; ++z) buf[xpos(ex2_cell(t, z), t >> 3)] = v[t][z];
   for (int t = 0; t < 64; ++t)
     for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
-  for (int t = 0; t < 64; ++t) inv_stageB(v[t], T2[t]);
+  for (int t = 0; t < 64; ++t) {
+    if (g_rec) inv_stageB(v[t], TwPow8(B2w[t]));
+    else inv_stageB(v[t], TabTw{T2[t]});
+  }
   for (int t = 0; t < 64; ++t)
     for (int z = 0; z < 8; ++z) buf[xpos(exB_cell(t, z), t & 7)] = v[t][z];
   for (int t = 0; t < 64; ++t)
     for (int s = 0; s < 8; ++s) v[t][s] = buf[xpos(t, s)];
   for (int t = 0; t < 64; ++t) {
-    inv_stageC(v[t], T1[t]);
+    if (g_rec) inv_stageC(v[t], TwPow8(B1b[t], B1w[t]));
+    else inv_stageC(v[t], TabTw{T1[t]});
     for (int a = 0; a < 8; ++a) {
+      for (double x : {v[t][a].x, v[t][a].y}) {
+        const double d = std::fabs(x - std::nearbyint(x));
+        if (d > *worst) *worst = d;
+      }
       out[t + 64 * a] = round_to_torus(v[t][a].x);
       out[t + 64 * a + 512] = round_to_torus(v[t][a].y);
     }
@@ -89,15 +116,9 @@ static bool check_swizzle() {
   return true;
 }
 
-int main(int argc, char** argv) {
-  int trials = argc > 1 ? atoi(argv[1]) : 20;
-  make_twiddles(T1, T2);
-  if (!check_swizzle()) {
-    printf("FAIL swizzle conflict\n");
-    return 1;
-  }
+static int run(int trials, bool rec, double* worst) {
+  g_rec = rec;
   std::mt19937_64 rng(7);
-  double worst = 0;
   for (int trial = 0; trial < trials; ++trial) {
     // 6 digit polys x 6 key polys summed, like one external-product output.
     std::vector<uint32_t> exact(1024, 0);
@@ -119,27 +140,39 @@ int main(int argc, char** argv) {
         bd[i] = double(int32_t(b[i])) / 512.0;
       }
       c64 D[64][8], B[64][8];
-      forward(dd.data(), D);
-      forward(bd.data(), B);
+      forward(dd.data(), D, rec);   // digit side: kernel's twiddle mode
+      forward(bd.data(), B, false);  // key side: tables (bk_to_fft_kernel)
       for (int t = 0; t < 64; ++t)
         for (int k = 0; k < 8; ++k) acc[t][k] = cadd(acc[t][k], cmul(D[t][k], B[t][k]));
     }
-    // distance to nearest integer of the un-rounded result
-    {
-      c64 v[64][8];
-      for (int t = 0; t < 64; ++t)
-        for (int k = 0; k < 8; ++k) v[t][k] = acc[t][k];
-      (void)v;
-    }
     std::vector<uint32_t> got(1024);
-    inverse(acc, got.data());
+    inverse(acc, got.data(), worst);
     for (int i = 0; i < 1024; ++i)
       if (got[i] != exact[i]) {
-        printf("FAIL trial %d coef %d got %u want %u\n", trial, i, got[i], exact[i]);
+        printf("FAIL (%s) trial %d coef %d got %u want %u\n", rec ? "rec" : "table", trial, i,
+               got[i], exact[i]);
         return 1;
       }
   }
-  (void)worst;
-  printf("OK %d trials bit-exact\n", trials);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  int trials = argc > 1 ? atoi(argv[1]) : 20;
+  make_twiddles(T1, T2);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int t = 0; t < 64; ++t) {
+    B1b[t] = T1[t][0];
+    B1w[t] = {double(std::cos(-pi * t / 256.0L)), double(std::sin(-pi * t / 256.0L))};
+    B2w[t] = {double(std::cos(-pi * (t >> 3) / 32.0L)), double(std::sin(-pi * (t >> 3) / 32.0L))};
+  }
+  if (!check_swizzle()) {
+    printf("FAIL swizzle conflict\n");
+    return 1;
+  }
+  double worst_tab = 0, worst_rec = 0;
+  if (run(trials, false, &worst_tab) || run(trials, true, &worst_rec)) return 1;
+  printf("OK %d trials bit-exact (table twiddles: max distance to integer %.4g; "
+         "generated twiddles: %.4g)\n", trials, worst_tab, worst_rec);
   return 0;
 }

@@ -1,7 +1,10 @@
 """Runs the kernel's FFT arithmetic (csrc/fft512.cuh, the same __host__
 __device__ functions) on the CPU with 64 emulated threads: exchange
-permutations, swizzle conflict-freedom and bit-exact negacyclic products."""
+permutations, swizzle conflict-freedom and bit-exact negacyclic products,
+with the table twiddles and with the generated twiddles (TwPow8) of the
+default throughput kernel; the rounding margin of both is asserted."""
 import os
+import re
 import shutil
 import subprocess
 
@@ -17,6 +20,10 @@ def test_fft_emulation_bit_exact(tmp_path):
                     "-I", os.path.join(REPO, "paper_2101_03403_b200", "csrc"),
                     os.path.join(REPO, "tests", "native", "fft_emul.cpp"), "-o", str(exe)],
                    check=True)
-    r = subprocess.run([str(exe), "30"], capture_output=True, text=True)
+    r = subprocess.run([str(exe), "60"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "bit-exact" in r.stdout
+    tab, rec = (float(x) for x in re.findall(r"twiddles: (?:max distance to integer )?([0-9.e-]+)",
+                                             r.stdout))
+    # a rounding flip needs 0.5; both modes keep a > 20x margin
+    assert tab < 0.025 and rec < 0.025, r.stdout

@@ -22,7 +22,7 @@ def main():
         ctx.set_profiling(rep > 0)
         ctx.reset_stats()
         t = time.perf_counter()
-        res, st = P.fu_batch(ctx, "add", 16, a, b)
+        res, st = P.fu_batch(ctx, os.environ.get("OP", "add"), 16, a, b)
         wall = (time.perf_counter() - t) * 1e3
         k = ctx.kernel_stats()
         print(f"rep {rep}: wall {wall:.1f} ms, device br {k['br_ms']:.1f} + ks {k['ks_ms']:.1f} ms,"
