@@ -148,7 +148,8 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * 3044 (G=4, 5) / v2 G=6 with per-thread twiddles generated on use (12
  * resident registers instead of 64); 9 = one bootstrap on 384
  * threads (six gadget rows concurrently, latency).  0 = auto (default): 9 for
- * levels up to 148 bootstraps, 13 up to 296, else 5044.  Every variant
+ * levels up to 148 bootstraps, 13 up to 296, else 5144 (5044 plus the
+ * rotated accumulator differences held across the gadget levels).  Every variant
  * computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);

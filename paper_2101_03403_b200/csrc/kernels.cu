@@ -20,6 +20,7 @@
 // All variants produce bit-identical ciphertexts (tests/test_gpu_parity.py).
 // DESIGN.md section 4 gives the roofline of each kernel; measured variant
 // comparisons are in profiles/.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -486,7 +487,7 @@ __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
 // tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
 // kTwRec: twiddles generated on use (TwPow8) -- 12 resident registers
 // instead of 64, so five bootstraps (10 warps) fit an SM's register file.
-template <int G, int S, bool kTmem = false, bool kTwRec = false>
+template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false>
 __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -576,24 +577,42 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
     c64 af[2][8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
+    // (X^ai - 1) * ACC at coefficients j and j + 512 of both parts, offset
+    // for the decomposition; kHold keeps the 32 words for the three gadget
+    // levels instead of re-reading the accumulator per level
+    auto rot_diff = [&](int x, uint32_t& da0, uint32_t& da1, uint32_t& db0, uint32_t& db1) {
+      const int j = t + 64 * x;
+      const int m0 = (j - ai) & (2 * kPolyN - 1);
+      const int m1 = (j + 512 - ai) & (2 * kPolyN - 1);
+      const uint32_t ra0 = m0 < kPolyN ? acc0[m0] : 0u - acc0[m0 - kPolyN];
+      const uint32_t ra1 = m1 < kPolyN ? acc0[m1] : 0u - acc0[m1 - kPolyN];
+      const uint32_t rb0 = m0 < kPolyN ? acc1[m0] : 0u - acc1[m0 - kPolyN];
+      const uint32_t rb1 = m1 < kPolyN ? acc1[m1] : 0u - acc1[m1 - kPolyN];
+      da0 = ra0 - acc0[j] + kDecompOffset;
+      da1 = ra1 - acc0[j + 512] + kDecompOffset;
+      db0 = rb0 - acc1[j] + kDecompOffset;
+      db1 = rb1 - acc1[j + 512] + kDecompOffset;
+    };
+    uint32_t dh[kHold ? 8 : 1][4];
+    if constexpr (kHold) {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) rot_diff(x, dh[x][0], dh[x][1], dh[x][2], dh[x][3]);
+    }
 #pragma unroll 1
     for (int p = 0; p < kL; ++p, q += 2) {
       const int shift = 32 - (p + 1) * kBgBit;
       c64 va[8], vb[8];
 #pragma unroll
       for (int x = 0; x < 8; ++x) {
-        // digits of (X^ai - 1) * ACC at coefficients j and j + 512, both parts
-        const int j = t + 64 * x;
-        const int m0 = (j - ai) & (2 * kPolyN - 1);
-        const int m1 = (j + 512 - ai) & (2 * kPolyN - 1);
-        const uint32_t ra0 = m0 < kPolyN ? acc0[m0] : 0u - acc0[m0 - kPolyN];
-        const uint32_t ra1 = m1 < kPolyN ? acc0[m1] : 0u - acc0[m1 - kPolyN];
-        const uint32_t rb0 = m0 < kPolyN ? acc1[m0] : 0u - acc1[m0 - kPolyN];
-        const uint32_t rb1 = m1 < kPolyN ? acc1[m1] : 0u - acc1[m1 - kPolyN];
-        const uint32_t da0 = ra0 - acc0[j] + kDecompOffset;
-        const uint32_t da1 = ra1 - acc0[j + 512] + kDecompOffset;
-        const uint32_t db0 = rb0 - acc1[j] + kDecompOffset;
-        const uint32_t db1 = rb1 - acc1[j + 512] + kDecompOffset;
+        uint32_t da0, da1, db0, db1;
+        if constexpr (kHold) {
+          da0 = dh[x][0];
+          da1 = dh[x][1];
+          db0 = dh[x][2];
+          db1 = dh[x][3];
+        } else {
+          rot_diff(x, da0, da1, db0, db1);
+        }
         va[x] = {u32_biased_to_double((da0 >> shift) & 127u, kDigitBias),
                  u32_biased_to_double((da1 >> shift) & 127u, kDigitBias)};
         vb[x] = {u32_biased_to_double((db0 >> shift) & 127u, kDigitBias),
@@ -732,6 +751,7 @@ struct WideSmem {
   uint64_t full[kRows];
 };
 
+template <bool kTwRec>
 __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -753,8 +773,10 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     mbar_expect_tx(&sm.full[g], kRowBytes);
     bulk_g2s(sm.bkbuf[g], bkf + (size_t)g * 1024, kRowBytes, &sm.full[g]);
   }
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
+  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
+  TwBases tb{};
+  if constexpr (kTwRec) tb = tw_bases(tw1, t);
+  else load_twiddles(tw1, tw2, t, T1, T2);
   prologue(job, slab, sm.bar, sm.acc[0], sm.acc[1], tid, 64 * kRows, cta_sync, 0);
   const int shift = 32 - (p + 1) * kBgBit;
   c64* xb = sm.xbuf[g];
@@ -767,10 +789,12 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     rotated_diff(sm.acc[part], ai, t, dif);
     c64 v[8];
     digits(dif, shift, v);
-    fwd_stage1(v, T1);
+    if constexpr (kTwRec) fwd_stage1(v, TwPow8(tb.t1b, tb.t1w));
+    else fwd_stage1(v, T1);
     exchange<1>(v, xb, t, sync);
     group_sync(bar_id);  // WAR on the single exchange buffer
-    fwd_stage2(v, T2);
+    if constexpr (kTwRec) fwd_stage2(v, TwPow8(tb.t2w));
+    else fwd_stage2(v, T2);
     exchange<2>(v, xb, t, sync);
     fwd_stage3(v);
     // partial products of this row with both output polynomials
@@ -811,14 +835,142 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
         v[k2] = cadd(cadd(sm.red[0][o][k2][t], sm.red[1][o][k2][t]), sm.red[2][o][k2][t]);
       inv_stageA(v);
       exchange<2>(v, sm.xbuf[g], t, sync);
-      inv_stageB(v, T2);
+      if constexpr (kTwRec) inv_stageB(v, TwPow8(tb.t2w));
+      else inv_stageB(v, T2);
       exchange<3>(v, sm.xbuf[g + 2], t, sync);
-      inv_stageC(v, T1);
+      if constexpr (kTwRec) inv_stageC(v, TwPow8(tb.t1b, tb.t1w));
+      else inv_stageC(v, T1);
       add_rounded(sm.acc[o], v, t);
     }
   }
   __syncthreads();
   extract(sm.acc[0], sm.acc[1], xout + (size_t)job.out * kXlweStride, tid, 64 * kRows);
+}
+
+// ------------------------------------ K1 + K2, latency: 2-SM cluster --
+// One bootstrap on a cluster of two CTAs (two SMs).  The wide kernel is bound
+// by one SM's shared-memory pipe (six transforms' exchanges, six key rows,
+// the partial-product reduction: LSU wavefronts 74% busy), so the work is
+// split by TRLWE part: CTA r holds ACC part r, transforms its three gadget
+// rows, and owns output polynomial r.  Its partial product for the other
+// output polynomial goes to the peer through distributed shared memory; one
+// cluster barrier per CMux step; each CTA then runs one inverse transform and
+// updates its own ACC part -- no ACC broadcast is needed, because the digits
+// of part r depend only on ACC part r.
+struct PairSmem {
+  c64 bkbuf[kL][1024];    // 48 KB: this CTA's three TRGSW rows
+  c64 xbuf[kL][512];      // 24 KB: one exchange buffer per group
+  c64 red[kL][2][8][64];  // 48 KB: partial products [p][o][k2][t]
+  c64 recv[2][8][64];     // 16 KB: the peer's partial for my polynomial (2 steps)
+  uint32_t acc[kPolyN];   // ACC part r
+  uint16_t bar[kLweWords + 1];
+  uint64_t full[kL];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
+    blind_rotate_pair_kernel(const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
+                             const c64* __restrict__ bkf, const c64* __restrict__ tw1,
+                             const c64* __restrict__ tw2, uint32_t* __restrict__ xout) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = int(cluster.block_rank());  // TRLWE part and output polynomial
+  const int tid = threadIdx.x;
+  const int g = tid >> 6, t = tid & 63;  // group g: gadget level g of part r
+  const int bar_id = 1 + g;
+  const BrJob job = jobs[blockIdx.x >> 1];
+  const int row = r * kL + g;  // TRGSW row (part * l + level)
+
+  if (tid == 0) {
+    for (int p = 0; p < kL; ++p) mbar_init(&sm.full[p], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (t == 0) {
+    mbar_expect_tx(&sm.full[g], kRowBytes);
+    bulk_g2s(sm.bkbuf[g], bkf + (size_t)row * 1024, kRowBytes, &sm.full[g]);
+  }
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
+  // K1: both CTAs mod-switch the input; each initialises its own ACC part
+  for (int i = tid; i < kLweWords; i += 64 * kL) {
+    uint32_t v = i == kN ? job.cst : 0u;
+    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
+    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
+    sm.bar[i] = (uint16_t)modswitch_2n(v);
+  }
+  __syncthreads();
+  {
+    const int barb = sm.bar[kN];
+    for (int j = tid; j < kPolyN; j += 64 * kL)
+      sm.acc[j] = r == 0 ? 0u : ((((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu));
+  }
+  c64* peer_recv = cluster.map_shared_rank(&sm.recv[0][0][0], r ^ 1);
+  const int shift = 32 - (g + 1) * kBgBit;
+  c64* xb = sm.xbuf[g];
+  auto sync = [bar_id] { group_sync(bar_id); };
+  cluster.sync();  // the peer's shared memory is live before any remote store
+
+  for (int i = 0; i < kN; ++i) {
+    __syncthreads();  // ACC part r of the previous step complete
+    const int ai = sm.bar[i];
+    uint32_t dif[16];
+    rotated_diff(sm.acc, ai, t, dif);
+    c64 v[8];
+    digits(dif, shift, v);
+    fwd_stage1(v, T1);
+    exchange<1>(v, xb, t, sync);
+    group_sync(bar_id);  // WAR on the single exchange buffer
+    fwd_stage2(v, T2);
+    exchange<2>(v, xb, t, sync);
+    fwd_stage3(v);
+    mbar_wait(&sm.full[g], i & 1);
+    const c64* bk = sm.bkbuf[g];
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      sm.red[g][0][k2][t] = cmul(v[k2], bk[k2 * 128 + t]);
+      sm.red[g][1][k2][t] = cmul(v[k2], bk[k2 * 128 + 64 + t]);
+    }
+    group_sync(bar_id);  // the group has read its key row
+    if (t == 0 && i + 1 < kN) {
+      mbar_expect_tx(&sm.full[g], kRowBytes);
+      bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + row) * 1024, kRowBytes,
+               &sm.full[g]);
+    }
+    __syncthreads();  // all three levels' partial products in red
+    if (g == 1) {     // the peer's polynomial: sum over levels, store remotely
+      c64* dst = peer_recv + (i & 1) * 512;
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2)
+        dst[k2 * 64 + t] = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
+                                sm.red[2][r ^ 1][k2][t]);
+    } else if (g == 0) {  // my polynomial: local part of the sum
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2)
+        v[k2] = cadd(cadd(sm.red[0][r][k2][t], sm.red[1][r][k2][t]), sm.red[2][r][k2][t]);
+    }
+    cluster.sync();  // partial products exchanged
+    if (g == 0) {
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) v[k2] = cadd(v[k2], sm.recv[i & 1][k2][t]);
+      inv_stageA(v);
+      exchange<2>(v, sm.xbuf[1], t, sync);
+      inv_stageB(v, T2);
+      exchange<3>(v, sm.xbuf[2], t, sync);
+      inv_stageC(v, T1);
+      add_rounded(sm.acc, v, t);
+    }
+  }
+  __syncthreads();
+  // sample extraction: CTA 0 owns a (from ACC part 0), CTA 1 the b word
+  uint32_t* out = xout + (size_t)job.out * kXlweStride;
+  if (r == 0) {
+    for (int j = tid; j < kPolyN; j += 64 * kL) out[j] = j == 0 ? sm.acc[0] : 0u - sm.acc[kPolyN - j];
+  } else if (tid == 0) {
+    out[kPolyN] = sm.acc[0];
+  }
+  cluster.sync();  // no CTA leaves while its shared memory may still be addressed
 }
 
 // ------------------------------------------------------------ K3 + K4 --
@@ -1189,26 +1341,39 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTmem = false, bool kTwRec = false>
+template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S>));
-  cudaError_t e = set_smem(blind_rotate_kernel_v3<G, S, kTmem, kTwRec>, smem, configured);
+  auto* kern = blind_rotate_kernel_v3<G, S, kTmem, kTwRec, kHold>;
+  cudaError_t e = set_smem(kern, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_kernel_v3<G, S, kTmem, kTwRec><<<(count + G - 1) / G, 64 * G, smem, s>>>(
-      jobs, count, slab, bkf, tw1, tw2, xout);
+  kern<<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
+template <bool kTwRec = false>
 static cudaError_t launch_wide(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(WideSmem));
-  cudaError_t e = set_smem(blind_rotate_wide_kernel, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_wide_kernel<kTwRec>, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_wide_kernel<<<count, 64 * kRows, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
+  blind_rotate_wide_kernel<kTwRec><<<count, 64 * kRows, smem, s>>>(jobs, slab, bkf, tw1, tw2,
+                                                                   xout);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_pair(const BrJob* jobs, int count, const uint32_t* slab,
+                               const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
+                               cudaStream_t s) {
+  static bool configured = false;
+  const int smem = int(sizeof(PairSmem));
+  cudaError_t e = set_smem(blind_rotate_pair_kernel, smem, configured);
+  if (e != cudaSuccess) return e;
+  blind_rotate_pair_kernel<<<2 * count, 64 * kL, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
@@ -1225,8 +1390,10 @@ int br_variant() {
 void set_br_variant(int v) { g_br_variant = v; }
 int default_br_variant() { return kDefaultBrVariant; }
 bool valid_br_variant(int v) {
-  return v == 0 || v == 1 || v == 9 || v == 13 || v == 22 || v == 23 || v == 43 || v == 3044 || v == 4044 ||
-         v == 5044 || v == 5054 || v == 5063;
+  return v == 0 || v == 1 || v == 9 || v == 19 || v == 92 || v == 13 || v == 22 || v == 23 ||
+         v == 43 ||
+         v == 3044 || v == 4044 ||
+         v == 5044 || v == 5054 || v == 5063 || v == 5144;
 }
 
 static int g_ks_variant = -1;
@@ -1243,26 +1410,29 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   if (count <= 0) return cudaSuccess;
   int variant = br_variant();
   if (variant == 0) {
-    // auto: a narrow level runs each bootstrap on a whole SM (latency); a
-    // level of up to two bootstraps per SM gives each its own CTA; wide
-    // levels use the throughput kernel (v3 with generated twiddles, 5044),
-    // whose SMs work in rounds of 4 bootstraps (~6.4 ms).  A last partial
-    // round of at most 2 bootstraps per SM is cheaper on the latency kernel
-    // (2 x 2.3 ms), so it is split off.
+    // auto: a very narrow level runs each bootstrap on a 2-SM cluster, a
+    // narrow one on a whole SM (latency); a level of up to two bootstraps
+    // per SM gives each its own CTA; wide
+    // levels use the throughput kernel (v3 with generated twiddles and held
+    // rotated differences, 5144), whose SMs work in rounds of 4 bootstraps
+    // (~6.3 ms).  A last partial round of at most 2 bootstraps per SM is
+    // cheaper on the latency kernel (2 x 2.3 ms), so it is split off.
     constexpr int kSms = 148, kRound = 4 * kSms;
-    if (count <= kSms) {
+    if (count <= kSms / 2) {
+      variant = 92;  // one bootstrap per 2-SM cluster: 1.62 vs 2.27 ms
+    } else if (count <= kSms) {
       variant = 9;
     } else if (count <= 2 * kSms) {
       variant = 13;
     } else {
       const int tail = count % kRound;
       if (tail > 0 && tail <= 2 * kSms && count > kRound) {
-        cudaError_t e =
-            launch_v3<4, 4, false, true>(jobs, count - tail, slab, bkf, tw1, tw2, xout, s);
+        cudaError_t e = launch_v3<4, 4, false, true, true>(jobs, count - tail, slab, bkf, tw1,
+                                                           tw2, xout, s);
         if (e != cudaSuccess) return e;
         return launch_wide(jobs + (count - tail), tail, slab, bkf, tw1, tw2, xout, s);
       }
-      variant = 5044;
+      variant = 5144;
     }
   }
   switch (variant) {
@@ -1270,6 +1440,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
       return cudaGetLastError();
     case 9: return launch_wide(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 19: return launch_wide<true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 92: return launch_pair(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 13: return launch_v2<1, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 22: return launch_v2<2, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
@@ -1279,6 +1451,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 4044: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 5044: return launch_v3<4, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 5054: return launch_v3<5, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5144:
+      return launch_v3<4, 4, false, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
