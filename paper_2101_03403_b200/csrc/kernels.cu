@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
 // of part r depend only on ACC part r.
 struct PairSmem {
   c64 bkbuf[kL][1024];    // 48 KB: this CTA's three TRGSW rows
-  c64 xbuf[kL][512];      // 24 KB: one exchange buffer per group
+  c64 xbuf[kL][2][512];   // 48 KB: two exchange buffers per group (no WAR barrier)
   c64 red[kL][2][8][64];  // 48 KB: partial products [p][o][k2][t]
   c64 recv[2][8][64];     // 16 KB: the peer's partial for my polynomial (2 steps)
   uint32_t acc[kPolyN];   // ACC part r
@@ -908,7 +908,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
   }
   c64* peer_recv = cluster.map_shared_rank(&sm.recv[0][0][0], r ^ 1);
   const int shift = 32 - (g + 1) * kBgBit;
-  c64* xb = sm.xbuf[g];
+  c64* xb0 = sm.xbuf[g][0];
+  c64* xb1 = sm.xbuf[g][1];
   auto sync = [bar_id] { group_sync(bar_id); };
   cluster.sync();  // the peer's shared memory is live before any remote store
 
@@ -920,10 +921,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     c64 v[8];
     digits(dif, shift, v);
     fwd_stage1(v, T1);
-    exchange<1>(v, xb, t, sync);
-    group_sync(bar_id);  // WAR on the single exchange buffer
+    exchange<1>(v, xb0, t, sync);
     fwd_stage2(v, T2);
-    exchange<2>(v, xb, t, sync);
+    exchange<2>(v, xb1, t, sync);
     fwd_stage3(v);
     mbar_wait(&sm.full[g], i & 1);
     const c64* bk = sm.bkbuf[g];
@@ -955,9 +955,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) v[k2] = cadd(v[k2], sm.recv[i & 1][k2][t]);
       inv_stageA(v);
-      exchange<2>(v, sm.xbuf[1], t, sync);
+      exchange<2>(v, sm.xbuf[1][0], t, sync);
       inv_stageB(v, T2);
-      exchange<3>(v, sm.xbuf[2], t, sync);
+      exchange<3>(v, sm.xbuf[2][0], t, sync);
       inv_stageC(v, T1);
       add_rounded(sm.acc, v, t);
     }
