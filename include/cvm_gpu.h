@@ -155,8 +155,9 @@ CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
 /* Key-switch kernel variant: 1 = one gate per CTA; 6 = one gate on 948
  * threads (6 position groups, latency); 7 = the level as one INT8
- * tensor-core product (one-hot digits x KSK byte limbs); 0 = auto (default:
- * 6 below 768 gates, else 7).  Bit-identical. */
+ * tensor-core product (one-hot digits x KSK byte limbs) on mma.sync; 8 = the
+ * same product on tcgen05.mma with the limb accumulators in tensor memory;
+ * 0 = auto (default: 6 below 256 gates, else 8).  Bit-identical. */
 CVM_API int cvm_set_ks_variant(int variant);
 CVM_API int cvm_get_ks_variant(void);
 

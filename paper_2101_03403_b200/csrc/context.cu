@@ -103,6 +103,7 @@ class Context {
     cudaFree(bkf_);
     cudaFree(ksk_);
     cudaFree(kskb_);
+    cudaFree(ksktc_);
     cudaFree(slab_);
     cudaFree(xlwe_);
     cudaFree(flush_buf_);
@@ -128,6 +129,9 @@ class Context {
           "upload ksk");
     if (!kskb_) check(cudaMalloc(&kskb_, kKskbWords * 4), "cudaMalloc(kskb)");
     check(launch_ksk_to_limbs(ksk_, kskb_, stream_), "ksk_to_limbs");
+    ++stats_.other_launches;
+    if (!ksktc_) check(cudaMalloc(&ksktc_, kKskTcWords * 4), "cudaMalloc(ksktc)");
+    check(launch_ksk_to_tc(ksk_, ksktc_, stream_), "ksk_to_tc");
     ++stats_.other_launches;
     check(cudaStreamSynchronize(stream_), "sync(upload_keys)");
     cudaFree(bk_tmp);
@@ -273,7 +277,7 @@ class Context {
           "blind_rotate_kernel");
     end_prof(p);
     p = begin_prof(1);
-    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, slab_, stream_),
+    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, ksktc_, slab_, stream_),
           "key_switch_kernel");
     end_prof(p);
     stats_.br_launches++;
@@ -501,7 +505,8 @@ class Context {
   cudaStream_t stream_ = nullptr;
   c64 *tw1_ = nullptr, *tw2_ = nullptr, *bkf_ = nullptr;
   uint32_t* ksk_ = nullptr;
-  uint32_t* kskb_ = nullptr;  // KSK as byte limbs for the tensor-core key switch
+  uint32_t* kskb_ = nullptr;   // KSK as byte limbs for the mma.sync key switch
+  uint32_t* ksktc_ = nullptr;  // the same limbs as tcgen05 B tiles
   uint32_t* slab_ = nullptr;
   uint64_t cap_ = 0;
   uint64_t used_ = 0;

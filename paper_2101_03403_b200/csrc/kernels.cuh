@@ -48,10 +48,11 @@ void set_br_variant(int v);
 bool valid_br_variant(int v);
 // Key-switch kernel: 1 = one gate per CTA; 6 = one gate per 948-thread CTA
 // (6 position groups, latency); 7 = the whole level as one INT8 tensor-core
-// product (one-hot digits x byte limbs of the KSK); 0 = auto by level width
-// (6 below kKsMmaMinGates gates, else 7).  Env CVM_KS_KERNEL.
+// product (one-hot digits x byte limbs of the KSK) on mma.sync; 8 = the same
+// product on tcgen05.mma with TMEM accumulators; 0 = auto by level width
+// (6 below kKsTcMinGates gates, else 8).  Env CVM_KS_KERNEL.
 constexpr int kDefaultKsVariant = 0;
-constexpr int kKsMmaMinGates = 768;
+constexpr int kKsTcMinGates = 256;
 int ks_variant();
 void set_ks_variant(int v);
 bool valid_ks_variant(int v);
@@ -62,8 +63,12 @@ cudaError_t launch_gather_lwe(const uint32_t* slab, const uint64_t* slots, uint6
 // launch_ksk_to_limbs from the padded [i][j][v][632] KSK.
 cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s);
 constexpr size_t kKskbWords = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
+// ksktc: the byte limbs pre-arranged as tcgen05 B tiles for variant 8
+// (1024 coefficients x 5 column tiles x 4 limbs x 4 KB).
+cudaError_t launch_ksk_to_tc(const uint32_t* ksk, uint32_t* ksktc, cudaStream_t s);
+constexpr size_t kKskTcWords = size_t(kPolyN) * 5 * 4 * 1024;
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
-                              const uint32_t* ksk, const uint32_t* kskb, uint32_t* slab,
-                              cudaStream_t s);
+                              const uint32_t* ksk, const uint32_t* kskb, const uint32_t* ksktc,
+                              uint32_t* slab, cudaStream_t s);
 
 }  // namespace cvm

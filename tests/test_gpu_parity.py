@@ -74,7 +74,7 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
-@pytest.mark.parametrize("ks_variant", [1, 6, 7])
+@pytest.mark.parametrize("ks_variant", [1, 6, 7, 8])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
     (two extracted samples + 1/8) and a partially filled last CTA."""
@@ -202,7 +202,7 @@ def test_key_switch_tensor_core_multi_tile(keyset, ctx):
     outs = {}
     old = lib.cvm_get_ks_variant()
     try:
-        for v in (6, 7):
+        for v in (6, 7, 8):
             check(lib.cvm_set_ks_variant(v))
             ctx.submit_level(gates)
             ctx.sync()
@@ -210,6 +210,7 @@ def test_key_switch_tensor_core_multi_tile(keyset, ctx):
     finally:
         check(lib.cvm_set_ks_variant(old))
     assert np.array_equal(outs[6], outs[7])
+    assert np.array_equal(outs[6], outs[8])
     bits = keyset.decrypt(outs[7])
     assert np.array_equal(bits[:n], np.where(s == 1, t, f))
     assert np.array_equal(bits[n:], 1 - (s ^ t))
