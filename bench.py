@@ -254,19 +254,27 @@ def extra_configs(P, ctx, ks):
     out["config1_nand4096"] = {"gates_per_s_device": n / ((k["br_ms"] + k["ks_ms"]) * 1e-3),
                                "device_ms": k["br_ms"] + k["ks_ms"], "correct": bool(ok)}
     # config 3: SUBS/CMP (sub + NZCV) and LSL by an encrypted amount, 256 each
+    def latency1(op, seed):
+        """Device time of one unit alone (batch 1: the latency kernels)."""
+        return fu(op, 1, seed)[3]["device_ms"]
+
     av, bv, res, d = fu("cmp", 256, 910)
     vals = ks.decrypt_words(res[:, :WIDTH].reshape(-1, 631), WIDTH)
     d["correct"] = bool(np.array_equal(vals, (av - bv) % (1 << WIDTH)))
+    d["latency_batch1_ms"] = latency1("cmp", 915)
     out["config3_cmp16"] = d
     av, bv, res, d = fu("lsl", 256, 920)
     vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
     d["correct"] = bool(np.array_equal(vals, (av << (bv % WIDTH)) % (1 << WIDTH)))
+    d["bootstraps_per_s_device"] = 2 * d["gates_per_s_device"]  # MUX = 2 bootstraps
+    d["latency_batch1_ms"] = latency1("lsl", 925)
     out["config3_lsl16"] = d
     # config 4: 64 x MUL16 producing the low 16 bits (the emulator's MUL):
     # the high half's 2,083 gates per multiplier are dead and never run
     av, bv, res, d = fu("mul_lo", 64, 930)
     vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
     d["correct"] = bool(np.array_equal(vals, (av * bv) % (1 << WIDTH)))
+    d["latency_batch1_ms"] = latency1("mul_lo", 935)
     out["config4_mul16"] = d
     av, bv, res, d = fu("umul", 64, 931)
     vals = ks.decrypt_words(res.reshape(-1, 631), 2 * WIDTH)
