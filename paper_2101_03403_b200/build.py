@@ -22,7 +22,9 @@ LIB = os.path.join(LIBDIR, "libcvm_b200.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-HOST_FLAGS = ["-O2", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall"]
+# (#pragma unroll in the shared __host__ __device__ FFT header is device-only)
+HOST_FLAGS = ["-O2", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall",
+              "-Wno-unknown-pragmas"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xptxas", "-v",
                      "--expt-relaxed-constexpr",
                      "-Xcompiler", ",".join(HOST_FLAGS)]
