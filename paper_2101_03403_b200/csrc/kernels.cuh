@@ -1,4 +1,5 @@
-// Device job descriptors and kernel launchers (see kernels.cu).
+// Device job descriptors and kernel launchers (blind_rotate.cu, key_switch.cu,
+// device_misc.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -59,7 +60,7 @@ bool valid_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
 cudaError_t launch_gather_lwe(const uint32_t* slab, const uint64_t* slots, uint64_t count,
                               uint32_t* out, cudaStream_t s);
-// kskb: the KSK as byte limbs for variant 7 (see kernels.cu), built by
+// kskb: the KSK as byte limbs for variant 7 (see key_switch.cu), built by
 // launch_ksk_to_limbs from the padded [i][j][v][632] KSK.
 cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s);
 constexpr size_t kKskbWords = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
