@@ -373,6 +373,19 @@ struct BrSmem3 {
   uint32_t tmem_base;
 };
 
+// chunk q (0 .. 6n-1, pair order) -> TRGSW row in the FFT-domain key
+__device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
+  const int i = q / 6, k = q - 6 * (q / 6);
+  const int row = (k & 1) * kL + (k >> 1);
+  return bkf + ((size_t)i * kRows + row) * 1024;
+}
+
+// kTmem: the key rows are copied once per CTA from the shared-memory ring
+// into a tensor-memory ring (tcgen05.cp, 64 columns per row, each thread's
+// bins in its own lane) and every bootstrap reads them with tcgen05.ld --
+// the G-fold shared-memory key reads leave the LSU path.  Thread 0 stages:
+// TMA row c -> smem slot c%4 -> (after the consumers released TMEM slot c%4)
+// tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
 // kTwRec: twiddles generated on use (TwPow8) -- 12 resident registers
 // instead of 64, so five bootstraps (10 warps) fit an SM's register file.
 template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false>

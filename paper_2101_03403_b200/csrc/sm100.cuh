@@ -62,7 +62,7 @@ __device__ __forceinline__ void group_sync(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-// ---- tcgen05 / TMEM helpers (v3 with the key ring in tensor memory) ----
+// ---- tcgen05 / tensor-memory helpers ----
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -109,20 +109,6 @@ __device__ __forceinline__ void tc_wait_ld16(uint32_t (&a)[8], uint32_t (&b)[8])
 __device__ __forceinline__ c64 c64_of(const uint32_t* r) {
   return {__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2])};
 }
-
-// chunk q (0 .. 6n-1, pair order) -> TRGSW row in the FFT-domain key
-__device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
-  const int i = q / 6, k = q - 6 * (q / 6);
-  const int row = (k & 1) * kL + (k >> 1);
-  return bkf + ((size_t)i * kRows + row) * 1024;
-}
-
-// kTmem: the key rows are copied once per CTA from the shared-memory ring
-// into a tensor-memory ring (tcgen05.cp, 64 columns per row, each thread's
-// bins in its own lane) and every bootstrap reads them with tcgen05.ld --
-// the G-fold shared-memory key reads leave the LSU path.  Thread 0 stages:
-// TMA row c -> smem slot c%4 -> (after the consumers released TMEM slot c%4)
-// tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
 
 // ---- cp.async (16-B copies, one commit group per stage) ----
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
