@@ -144,6 +144,15 @@ void ff_forward_u32(const uint32_t* in, double* out) {
   forward_d(p, out);
 }
 
+/* round(v) mod 2^32 for |v| < 2^51 (round half to even, like llrint): add
+ * 1.5 * 2^52 and keep the low mantissa word -- vectorisable, unlike llrint. */
+static inline uint32_t round_torus(double v) {
+  const double t = v + 6755399441055744.0;
+  uint64_t bits;
+  memcpy(&bits, &t, 8);
+  return (uint32_t)bits;
+}
+
 void ff_inverse_round(const double* in, uint32_t* out) {
   double re[M], im[M];
   memcpy(re, in, sizeof(re));
@@ -154,7 +163,7 @@ void ff_inverse_round(const double* in, uint32_t* out) {
     const double zr = re[j] * s, zi = im[j] * s;
     const double wr = zr * tw_re[j] + zi * tw_im[j];
     const double wi = zi * tw_re[j] - zr * tw_im[j];
-    out[j] = (uint32_t)(int64_t)llrint(wr);
-    out[j + M] = (uint32_t)(int64_t)llrint(wi);
+    out[j] = round_torus(wr);
+    out[j + M] = round_torus(wi);
   }
 }

@@ -565,6 +565,121 @@ static void* worker(void* arg) {
   return NULL;
 }
 
+/* ---- batched lockstep evaluation (the CPU speed baseline) ----------------
+ * The per-gate worker above streams the whole bootstrapping key (62 MB in FFT
+ * domain) once per gate per thread, so many threads are DRAM-bound.  Batched
+ * the way the GPU runs a level: every bootstrap of the batch advances one CMux
+ * step at a time, all threads on the same key row (96 KB, cache-resident
+ * across the thread's bootstraps), one barrier per step. */
+typedef struct {
+  uint32_t acc[2][N];
+  uint16_t bar[NL + 1];
+} brstate_t;
+
+typedef struct {
+  const oracle_keys* k;
+  brstate_t* st;
+  int nboot, tid, nthreads;
+  pthread_barrier_t* barrier;
+  /* epilogue: gates g = tid, tid + nthreads, ... (first[g] = its bootstrap) */
+  int count;
+  const uint8_t* kinds;
+  const int* first;
+  uint32_t* out;
+} lockstep_t;
+
+static void lockstep_extract(const brstate_t* st, uint32_t* out);
+
+static void* lockstep_worker(void* arg) {
+  lockstep_t* L = (lockstep_t*)arg;
+  scratch_t* s = (scratch_t*)malloc(sizeof(scratch_t));
+  for (int i = 0; i < NL; ++i) {
+    for (int j = L->tid; j < L->nboot; j += L->nthreads) {
+      const int a = L->st[j].bar[i];
+      if (a) cmux_step(L->k, i, L->st[j].acc, a, s);
+    }
+    pthread_barrier_wait(L->barrier);
+  }
+  free(s);
+  /* extraction + key switch (MUX: both extractions + (0, 1/8)) */
+  for (int g = L->tid; g < L->count; g += L->nthreads) {
+    uint32_t x1[OR_XLWE_WORDS], x2[OR_XLWE_WORDS];
+    const int j = L->first[g];
+    lockstep_extract(&L->st[j], x1);
+    if (L->kinds[g] == OR_MUX) {
+      lockstep_extract(&L->st[j + 1], x2);
+      for (int q = 0; q < OR_XLWE_WORDS; ++q) x1[q] += x2[q];
+      x1[N] += 1u << 29;
+    }
+    oracle_key_switch(L->k, x1, L->out + (size_t)g * OR_LWE_WORDS);
+  }
+  return NULL;
+}
+
+static void lockstep_init(brstate_t* st, const uint32_t* lwe) {
+  uint32_t tv[N];
+  for (int j = 0; j < N; ++j) tv[j] = MU;
+  for (int i = 0; i <= NL; ++i) st->bar[i] = (uint16_t)oracle_modswitch(lwe[i]);
+  memset(st->acc[0], 0, sizeof(st->acc[0]));
+  mul_xai(st->acc[1], (2 * N - st->bar[NL]) % (2 * N), tv);
+}
+
+static void lockstep_extract(const brstate_t* st, uint32_t* out) {
+  out[0] = st->acc[0][0];
+  for (int j = 1; j < N; ++j) out[j] = 0u - st->acc[0][N - j];
+  out[N] = st->acc[1][0];
+}
+
+static int gates_lockstep(const oracle_keys* k, int count, const uint8_t* kinds,
+                          const uint32_t* in_a, const uint32_t* in_b, const uint32_t* in_c,
+                          uint32_t* out, int threads) {
+  int nboot = 0;
+  int* first = (int*)malloc(sizeof(int) * (size_t)(count > 0 ? count : 1));
+  if (!first) return -1;
+  for (int g = 0; g < count; ++g) {
+    first[g] = nboot;
+    nboot += kinds[g] == OR_MUX ? 2 : 1;
+  }
+  brstate_t* st = (brstate_t*)malloc(sizeof(brstate_t) * (size_t)(nboot > 0 ? nboot : 1));
+  if (!st) {
+    free(first);
+    return -1;
+  }
+  uint32_t t[OR_LWE_WORDS];
+  for (int g = 0, j = 0; g < count; ++g) {
+    const size_t o = (size_t)g * OR_LWE_WORDS;
+    if (kinds[g] == OR_MUX) {
+      const uint32_t e = 1u << 29;
+      combine(0u - e, 1, in_a + o, 1, in_b + o, t);
+      lockstep_init(&st[j++], t);
+      combine(0u - e, -1, in_a + o, 1, in_c + o, t);
+      lockstep_init(&st[j++], t);
+    } else {
+      uint32_t cst;
+      int ca, cb;
+      gate_combo(kinds[g], &cst, &ca, &cb);
+      combine(cst, ca, in_a + o, cb, in_b + o, t);
+      lockstep_init(&st[j++], t);
+    }
+  }
+  if (threads > nboot) threads = nboot > 0 ? nboot : 1;
+  if (threads > 256) threads = 256;
+  pthread_barrier_t barrier;
+  pthread_barrier_init(&barrier, NULL, (unsigned)threads);
+  pthread_t tid[256];
+  lockstep_t L[256];
+  for (int i = 0; i < threads; ++i) {
+    L[i] = (lockstep_t){k, st, nboot, i, threads, &barrier, count, kinds, first, out};
+    if (i > 0) pthread_create(&tid[i], NULL, lockstep_worker, &L[i]);
+  }
+  lockstep_worker(&L[0]);
+  for (int i = 1; i < threads; ++i) pthread_join(tid[i], NULL);
+  pthread_barrier_destroy(&barrier);
+  free(st);
+  free(first);
+  return 0;
+}
+
 int oracle_gates(const oracle_keys* k, int count, const uint8_t* kinds,
                  const uint32_t* in_a, const uint32_t* in_b,
                  const uint32_t* in_c, uint32_t* out, int threads) {
@@ -573,6 +688,8 @@ int oracle_gates(const oracle_keys* k, int count, const uint8_t* kinds,
   for (int g = 0; g < count; ++g)
     if (kinds[g] < OR_NAND || kinds[g] > OR_MUX || (kinds[g] == OR_MUX && !in_c))
       return -1;
+  if (k->mode == OR_MODE_FFT && count > 1)
+    return gates_lockstep(k, count, kinds, in_a, in_b, in_c, out, threads < 1 ? 1 : threads);
   if (threads < 1) threads = 1;
   if (threads > count) threads = count > 0 ? count : 1;
   pthread_t tid[256];
