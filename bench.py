@@ -172,10 +172,10 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     sk = O.SecretKeys(KEY_SEED)
     ck = O.CloudKeys(sk.bk, sk.ksk, O.MODE_FFT)
-    # 8 gates per thread per step: long enough that thread start-up does not
-    # depress the CPU rate (2 per thread measured ~25% low), short enough for
-    # a few-minute run
-    n = threads * int(os.environ.get("REF_ROUNDS", "8"))
+    # 32 gates per thread per step, evaluated in lockstep (the oracle's batched
+    # mode): enough bootstraps that thread start-up and the per-CMux-step
+    # barrier do not depress the CPU rate, short enough for a few-minute run
+    n = threads * int(os.environ.get("REF_ROUNDS", "32"))
     kinds, a, b = cpu_sample_inputs(sk, n)
     for _ in range(args.warmup):
         ck.gates(kinds[:threads], a[:threads], b[:threads], threads=threads)
