@@ -310,6 +310,7 @@ class Context {
     if (!has_keys_) throw StateError("plan before upload_keys");
     check(cudaSetDevice(device_), "cudaSetDevice");
     auto plan = std::make_unique<Plan>();
+    plan->owner = this;
     size_t bytes = 0;
     std::vector<uint64_t> nbr(levels.size());
     for (size_t l = 0; l < levels.size(); ++l) {
@@ -339,6 +340,8 @@ class Context {
   }
 
   void run_plan(Plan* p, bool graph) {
+    // job tables and slots live on the context that captured the plan
+    if (p->owner != this) throw InputError("plan_run: plan was captured on another context");
     check(cudaSetDevice(device_), "cudaSetDevice");
     if (p->max_br > xcap_) grow_xlwe(p->max_br);
     if (!graph || profiling) {

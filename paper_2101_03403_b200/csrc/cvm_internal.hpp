@@ -55,6 +55,7 @@ struct Plan {
   void* exec = nullptr;  // cudaGraphExec_t
   const void* graph_slab = nullptr;
   const void* graph_xlwe = nullptr;
+  const Context* owner = nullptr;  // the context whose slots and memory it uses
 };
 Context* context_create(int device);
 void context_destroy(Context* c);

@@ -129,3 +129,18 @@ def test_concurrent_recording_threads(keyset, ctx):
     got = bk.decrypt_bits(np.array(outs, np.uint64).ravel()).reshape(n_threads, per)
     want = 1 - ((xs[..., 0] ^ xs[..., 1]) & xs[..., 0])
     assert np.array_equal(got, want)
+
+
+def test_plan_rejects_foreign_context(keyset, ctx):
+    """A plan's job tables and slots belong to the context that captured it."""
+    bk = P.Backend(ctx, keyset)
+    bk.binary_gate("AND", bk.encrypt_bit(1), bk.encrypt_bit(1))
+    plan = bk.capture_plan()
+    other = P.Context(0)
+    try:
+        with pytest.raises(CvmInputError):
+            plan.run(other)
+    finally:
+        other.close()
+    plan.run(ctx)  # its own context still works
+    ctx.sync()
