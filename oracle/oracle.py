@@ -175,28 +175,40 @@ def eval_dag(ck, nodes, inputs, threads=None):
     """
     n = len(nodes)
     ct = np.zeros((n, LWE_WORDS), np.uint32)
+    done = np.zeros(n, bool)
     lv = dag_levels(nodes)
     k_in = 0
     order = np.argsort(lv, kind="stable")
-    # free ops / inputs must respect id order inside a level: process by level,
-    # within a level first free ops in id order (their deps are lower levels or
-    # earlier free ops), then the bootstrapped batch.
+
+    def free_op(i):
+        kind, inp, nd, d0, d1, d2, val = nodes[i]
+        if kind == CONSTANT:
+            ct[i] = trivial(bool(val))
+        elif kind == NOT:
+            ct[i] = (np.uint32(0) - ct[d0 - 1]).astype(np.uint32)
+        else:  # COPY
+            ct[i] = ct[d0 - 1]
+        done[i] = True
+
+    # By level.  A free op (NOT / COPY) shares the level of the gate it reads,
+    # so inside a level: inputs and the free ops whose operand is ready, in id
+    # order; then the bootstrapped batch; then the remaining free ops in id
+    # order (they read this batch or earlier free ops of the same pass).
     for level in range(int(lv.max()) + 1 if n else 0):
         ids = order[lv[order] == level]
-        boot = []
+        boot, later = [], []
         for i in ids:
-            kind, inp, nd, d0, d1, d2, val = nodes[i]
+            kind, inp, nd, d0 = nodes[i][:4]
             if inp:
                 ct[i] = inputs[k_in]
                 k_in += 1
-            elif kind == CONSTANT:
-                ct[i] = trivial(bool(val))
-            elif kind == NOT:
-                ct[i] = (np.uint32(0) - ct[d0 - 1]).astype(np.uint32)
-            elif kind == COPY:
-                ct[i] = ct[d0 - 1]
-            else:
+                done[i] = True
+            elif kind >= NAND:
                 boot.append(i)
+            elif kind == CONSTANT or done[d0 - 1]:
+                free_op(i)
+            else:
+                later.append(i)
         if boot:
             boot = np.array(boot)
             kinds = nodes[boot, 0].astype(np.uint8)
@@ -204,4 +216,7 @@ def eval_dag(ck, nodes, inputs, threads=None):
             b = ct[nodes[boot, 4] - 1]
             c = ct[np.maximum(nodes[boot, 5], 1) - 1]
             ct[boot] = ck.gates(kinds, a, b, c, threads)
+            done[boot] = True
+        for i in later:
+            free_op(i)
     return ct

@@ -113,3 +113,21 @@ def test_rejects_non_bootstrapped_kind(sk, ck_ntt):
     a = sk.encrypt(np.array([1], np.uint8), 1)
     with pytest.raises(ValueError):
         ck_ntt.gates(np.array([O.NOT], np.uint8), a, a)
+
+
+def test_eval_dag_free_ops_after_same_level_gates(sk, ck_ntt):
+    """A NOT / COPY shares the dataflow level of the gate it reads: eval_dag
+    must run it after that level's bootstrapped batch (regression: it once
+    read the gate's output before it was computed)."""
+    I, C, NT, CP, AND, XOR = 1, O.CONSTANT, O.NOT, O.COPY, O.AND, O.XOR
+    # ids: 1 a, 2 b, 3 AND(a,b), 4 COPY(3), 5 NOT(3), 6 XOR(4,5), 7 NOT(4)
+    nodes = np.array([[C, I, 0, 0, 0, 0, 0], [C, I, 0, 0, 0, 0, 0],
+                      [AND, 0, 2, 1, 2, 0, 0], [CP, 0, 1, 3, 0, 0, 0],
+                      [NT, 0, 1, 3, 0, 0, 0], [XOR, 0, 2, 4, 5, 0, 0],
+                      [NT, 0, 1, 4, 0, 0, 0]], np.int64)
+    ins = sk.encrypt(np.array([1, 1], np.uint8), 5)
+    ct = O.eval_dag(ck_ntt, nodes, ins)
+    assert np.array_equal(ct[3], ct[2])
+    assert np.array_equal(ct[4], (np.uint32(0) - ct[2]).astype(np.uint32))
+    assert np.array_equal(ct[6], ct[4])
+    assert list(sk.decrypt(ct[2:])) == [1, 1, 0, 1, 0]
