@@ -247,3 +247,27 @@ def test_random_circuits_bit_exact(seed, keyset, ctx, oracle_keys):
     ref = O.eval_dag(oracle_keys, nodes, cins)
     got = bk.export_lwe(np.arange(1, len(nodes) + 1, dtype=np.uint64))
     assert np.array_equal(got, ref)
+
+
+def test_random_wide_levels_bit_exact(keyset, ctx, oracle_keys):
+    """Two random 320-gate levels (binary gates and MUX mixed, operands with
+    folded NOT / COPY): wide enough for the throughput kernel and the tcgen05
+    key switch; every node bit-exact against the oracle."""
+    rng = np.random.default_rng(99)
+    bits = rng.integers(0, 2, 16).astype(np.uint8)
+    cins = keyset.encrypt(bits, 400)
+    bk = P.Backend(ctx, keyset)
+    layer = [int(h) for h in bk.import_lwe(cins)]
+    kinds = list(TRUTH) + ["MUX"]
+    for _ in range(2):
+        src = layer + [int(bk.unary_gate("NOT", h)) for h in layer[:8]]
+        nxt = []
+        for _ in range(320):
+            k = kinds[rng.integers(len(kinds))]
+            pick = [src[i] for i in rng.integers(0, len(src), 3)]
+            nxt.append(int(bk.mux_gate(*pick) if k == "MUX" else bk.binary_gate(k, *pick[:2])))
+        layer = nxt
+    nodes = bk.nodes()
+    ref = O.eval_dag(oracle_keys, nodes, cins)
+    got = bk.export_lwe(np.arange(1, len(nodes) + 1, dtype=np.uint64))
+    assert np.array_equal(got, ref)
