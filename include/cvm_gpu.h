@@ -146,10 +146,13 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * per CTA, two transforms in flight per thread; 4044 = 3044 with the key
  * ring in tensor memory (tcgen05.cp / tcgen05.ld); 5044 / 5054 / 5063 =
  * 3044 (G=4, 5) / v2 G=6 with per-thread twiddles generated on use (12
- * resident registers instead of 64); 9 = one bootstrap on 384
- * threads (six gadget rows concurrently, latency).  0 = auto (default): 9 for
- * levels up to 148 bootstraps, 13 up to 296, else 5144 (5044 plus the
- * rotated accumulator differences held across the gadget levels).  Every variant
+ * resident registers instead of 64); 5144 / 5146 = 5044 plus the rotated
+ * accumulator differences held across the gadget levels (4- / 6-row key
+ * ring); 5244 / 5245 / 5246 / 5247 = 5144 with each key slot refilled by its
+ * last reader (4- to 7-row ring); 9 = one bootstrap on 384 threads (six
+ * gadget rows concurrently, latency); 19 = 9 with generated twiddles; 92 = one
+ * bootstrap on a 2-SM thread-block cluster.  0 = auto (default): 92 for levels
+ * up to 74 bootstraps, 9 up to 148, 13 up to 296, else 5247.  Every variant
  * computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);

@@ -370,6 +370,7 @@ struct BrSmem3 {
   uint16_t bar[G][kLweWords + 1];
   uint64_t full[S], empty[S];
   uint64_t tfull[S], tempty[S];  // TMEM key ring (kTmem)
+  uint32_t cnt[S];               // readers done with each slot (kLast)
   uint32_t tmem_base;
 };
 
@@ -388,7 +389,8 @@ __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
 // tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
 // kTwRec: twiddles generated on use (TwPow8) -- 12 resident registers
 // instead of 64, so five bootstraps (10 warps) fit an SM's register file.
-template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false>
+template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false,
+          bool kLast = false>
 __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
       mbar_init(&sm.empty[s], 64 * G);
       mbar_init(&sm.tfull[s], 1);
       mbar_init(&sm.tempty[s], 64 * G);
+      sm.cnt[s] = 0;
     }
     mbar_init_fence();
   }
@@ -542,7 +545,8 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
       const int sa = q % S, sb = (q + 1) % S;
       if constexpr (!kTmem) {
         // producer: refill the slots of chunks q-2, q-1 with chunks q+S-2, q+S-1
-        if (tid == 0) {
+        // (kLast: the last consumer of a slot refills it instead, below)
+        if (!kLast && tid == 0) {
 #pragma unroll
           for (int c = q - 2; c < q; ++c) {
             if (c < 0 || c + S >= kChunks) continue;
@@ -563,8 +567,25 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
           af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
           af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
         }
-        mbar_arrive(&sm.empty[sa]);
-        mbar_arrive(&sm.empty[sb]);
+        if constexpr (!kLast) {
+          mbar_arrive(&sm.empty[sa]);
+          mbar_arrive(&sm.empty[sb]);
+        } else {
+          // the slot's last reader streams the chunk S ahead into it at once,
+          // so no thread blocks waiting for the slowest bootstrap
+          __threadfence_block();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int slot = h ? sb : sa, c = q + h;
+            if (atomicAdd(&sm.cnt[slot], 1u) == 64u * G - 1u) {
+              sm.cnt[slot] = 0;
+              if (c + S < kChunks) {
+                mbar_expect_tx(&sm.full[slot], kRowBytes);
+                bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+              }
+            }
+          }
+        }
       } else {
         mbar_wait(&sm.tfull[sa], (q >> 2) & 1);
         mbar_wait(&sm.tfull[sb], ((q + 1) >> 2) & 1);
@@ -893,12 +914,13 @@ static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false>
+template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false,
+          bool kLast = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(BrSmem3<G, S>));
-  auto* kern = blind_rotate_kernel_v3<G, S, kTmem, kTwRec, kHold>;
+  auto* kern = blind_rotate_kernel_v3<G, S, kTmem, kTwRec, kHold, kLast>;
   cudaError_t e = set_smem(kern, smem, configured);
   if (e != cudaSuccess) return e;
   kern<<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf, tw1, tw2, xout);
@@ -940,7 +962,8 @@ bool valid_br_variant(int v) {
   return v == 0 || v == 1 || v == 9 || v == 19 || v == 92 || v == 13 || v == 22 || v == 23 ||
          v == 43 ||
          v == 3044 || v == 4044 ||
-         v == 5044 || v == 5054 || v == 5063 || v == 5144;
+         v == 5044 || v == 5054 || v == 5063 || v == 5144 || v == 5146 || v == 5244 ||
+         v == 5245 || v == 5246 || v == 5247;
 }
 
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
@@ -952,10 +975,11 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     // auto: a very narrow level runs each bootstrap on a 2-SM cluster, a
     // narrow one on a whole SM (latency); a level of up to two bootstraps
     // per SM gives each its own CTA; wide
-    // levels use the throughput kernel (v3 with generated twiddles and held
-    // rotated differences, 5144), whose SMs work in rounds of 4 bootstraps
-    // (~6.3 ms).  A last partial round of at most 2 bootstraps per SM is
-    // cheaper on the latency kernel (2 x 2.3 ms), so it is split off.
+    // levels use the throughput kernel (v3 with generated twiddles, held
+    // rotated differences, a 7-row key ring refilled by each slot's last
+    // reader: 5247), whose SMs work in rounds of 4 bootstraps (~5.9 ms).  A
+    // last partial round of at most 2 bootstraps per SM is cheaper on the
+    // latency kernel (2 x 2.3 ms), so it is split off.
     constexpr int kSms = 148, kRound = 4 * kSms;
     if (count <= kSms / 2) {
       variant = 92;  // one bootstrap per 2-SM cluster: 1.62 vs 2.27 ms
@@ -966,12 +990,12 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     } else {
       const int tail = count % kRound;
       if (tail > 0 && tail <= 2 * kSms && count > kRound) {
-        cudaError_t e = launch_v3<4, 4, false, true, true>(jobs, count - tail, slab, bkf, tw1,
-                                                           tw2, xout, s);
+        cudaError_t e = launch_v3<4, 7, false, true, true, true>(jobs, count - tail, slab, bkf,
+                                                                 tw1, tw2, xout, s);
         if (e != cudaSuccess) return e;
         return launch_wide(jobs + (count - tail), tail, slab, bkf, tw1, tw2, xout, s);
       }
-      variant = 5144;
+      variant = 5247;
     }
   }
   switch (variant) {
@@ -992,6 +1016,16 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 5054: return launch_v3<5, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 5144:
       return launch_v3<4, 4, false, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5146:
+      return launch_v3<4, 6, false, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5244:  // 5144 + the last reader of a key slot refills it
+      return launch_v3<4, 4, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5245:
+      return launch_v3<4, 5, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5246:
+      return launch_v3<4, 6, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5247:
+      return launch_v3<4, 7, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }
