@@ -571,17 +571,21 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
           mbar_arrive(&sm.empty[sa]);
           mbar_arrive(&sm.empty[sb]);
         } else {
-          // the slot's last reader streams the chunk S ahead into it at once,
-          // so no thread blocks waiting for the slowest bootstrap
-          __threadfence_block();
+          // the slot's last reader (counted per warp) streams the chunk S
+          // ahead into it at once, so no thread blocks waiting for the
+          // slowest bootstrap
+          __syncwarp();
+          if ((tid & 31) == 0) {
+            __threadfence_block();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int slot = h ? sb : sa, c = q + h;
-            if (atomicAdd(&sm.cnt[slot], 1u) == 64u * G - 1u) {
-              sm.cnt[slot] = 0;
-              if (c + S < kChunks) {
-                mbar_expect_tx(&sm.full[slot], kRowBytes);
-                bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+            for (int h = 0; h < 2; ++h) {
+              const int slot = h ? sb : sa, c = q + h;
+              if (atomicAdd(&sm.cnt[slot], 32u) == 64u * G - 32u) {
+                sm.cnt[slot] = 0;
+                if (c + S < kChunks) {
+                  mbar_expect_tx(&sm.full[slot], kRowBytes);
+                  bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
+                }
               }
             }
           }

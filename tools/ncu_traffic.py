@@ -32,7 +32,8 @@ def main():
                      "gpu__time_duration.sum --clock-control none, python bench.py --steps 1 "
                      "--warmup 1 --no-cpu --no-extras (tools/ncu_traffic.py); per launch"}
     groups = {"blind_rotate_v3": "blind_rotate_kernel_v3", "blind_rotate_wide": "wide_kernel",
-              "blind_rotate_pair": "pair_kernel", "key_switch_mma": "key_switch_mma"}
+              "blind_rotate_pair": "pair_kernel", "key_switch_mma": "key_switch_mma",
+              "key_switch_tc": "key_switch_tc", "key_switch_wide": "key_switch_wide"}
     for name, pat in groups.items():
         ls = [d for d in launches.values() if pat in d["kernel"]]
         if not ls:
