@@ -24,17 +24,12 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "br_common.cuh"
 #include "fft512.cuh"
 #include "kernels.cuh"
 #include "sm100.cuh"
 
 namespace cvm {
-
-// digits: buf = c + offset; d_p = ((buf >> (25 - 7p)) & 127) - 64
-constexpr uint32_t kDecompOffset =
-    (1u << (kBgBit - 1)) * ((1u << 25) + (1u << 18) + (1u << 11));
-constexpr double kDigitBias = 4503599627370496.0 + 64.0;  // 2^52 + Bg/2
-constexpr uint32_t kRowBytes = 1024 * 16;                 // one TRGSW row, FFT domain
 
 __device__ __forceinline__ void load_twiddles(const c64* tw1, const c64* tw2, int t,
                                               c64 T1[8], c64 T2[8]) {
@@ -83,33 +78,6 @@ __device__ __forceinline__ void exchange_pair(c64 va[8], c64 vb[8], c64* ba, c64
     vb[s] = bb[xpos(t, s)];
   }
   group_sync(bar_id);
-}
-
-// K1: the gate's input sample (cst + coef0*slot0 + coef1*slot1) mod-switched
-// to Z_2N, then ACC = X^{-b} (0, mu * sum X^j).
-__device__ __forceinline__ void prologue(const BrJob& job, const uint32_t* slab, uint16_t* bar,
-                                         uint32_t* acc0, uint32_t* acc1, int t, int nthreads,
-                                         void (*sync)(int), int sync_arg) {
-  for (int i = t; i < kLweWords; i += nthreads) {
-    uint32_t v = i == kN ? job.cst : 0u;
-    if (job.coef[0]) v += (uint32_t)job.coef[0] * slab[(size_t)job.slot[0] * kLweStride + i];
-    if (job.coef[1]) v += (uint32_t)job.coef[1] * slab[(size_t)job.slot[1] * kLweStride + i];
-    bar[i] = (uint16_t)modswitch_2n(v);
-  }
-  sync(sync_arg);
-  const int barb = bar[kN];
-  for (int j = t; j < kPolyN; j += nthreads) {
-    acc0[j] = 0;
-    acc1[j] = (((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu);
-  }
-}
-__device__ void cta_sync(int) { __syncthreads(); }
-
-// Sample extraction: a'_0 = a_0, a'_j = -a_{N-j}, b' = b_0.
-__device__ __forceinline__ void extract(const uint32_t* acc0, const uint32_t* acc1,
-                                        uint32_t* out, int t, int nthreads) {
-  for (int j = t; j < kPolyN; j += nthreads) out[j] = j == 0 ? acc0[0] : 0u - acc0[kPolyN - j];
-  if (t == 0) out[kPolyN] = acc1[0];
 }
 
 // 16 digit-pairs of (X^ai - 1) * ACC_part owned by thread t (coefficients
@@ -967,14 +935,17 @@ bool valid_br_variant(int v) {
          v == 43 ||
          v == 3044 || v == 4044 ||
          v == 5044 || v == 5054 || v == 5063 || v == 5144 || v == 5146 || v == 5244 ||
-         v == 5245 || v == 5246 || v == 5247;
+         v == 5245 || v == 5246 || v == 5247 || valid_br_v4_variant(v);
 }
 
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
-                                uint32_t* xout, cudaStream_t s) {
+                                const c64* bkf4, const c64* tw4, uint32_t* xout,
+                                cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   int variant = br_variant();
+  if (valid_br_v4_variant(variant))
+    return launch_blind_rotate_v4(variant, jobs, count, slab, bkf4, tw4, xout, s);
   if (variant == 0) {
     // auto: a very narrow level runs each bootstrap on a 2-SM cluster, a
     // narrow one on a whole SM (latency); a level of up to two bootstraps

@@ -86,6 +86,14 @@ class Context {
     check(cudaMalloc(&tw2_, sizeof(T2)), "cudaMalloc(tw2)");
     check(cudaMemcpy(tw1_, T1, sizeof(T1), cudaMemcpyHostToDevice), "tw1");
     check(cudaMemcpy(tw2_, T2, sizeof(T2), cudaMemcpyHostToDevice), "tw2");
+    c64 T4[32][2];  // warp FFT (v4) per-lane twiddle bases
+    for (int l = 0; l < 32; ++l) {
+      const TwBasesW b = make_wbases(l);
+      T4[l][0] = b.base;
+      T4[l][1] = b.w;
+    }
+    check(cudaMalloc(&tw4_, sizeof(T4)), "cudaMalloc(tw4)");
+    check(cudaMemcpy(tw4_, T4, sizeof(T4), cudaMemcpyHostToDevice), "tw4");
     check(cudaEventCreate(&ev_user_[0]), "event");
     check(cudaEventCreate(&ev_user_[1]), "event");
   }
@@ -100,7 +108,9 @@ class Context {
     cudaEventDestroy(ev_user_[1]);
     cudaFree(tw1_);
     cudaFree(tw2_);
+    cudaFree(tw4_);
     cudaFree(bkf_);
+    cudaFree(bkf4_);
     cudaFree(ksk_);
     cudaFree(kskb_);
     cudaFree(ksktc_);
@@ -121,6 +131,10 @@ class Context {
     check(cudaMemcpyAsync(bk_tmp, bk, kBkWords * 4, cudaMemcpyHostToDevice, stream_),
           "upload bk");
     check(launch_bk_to_fft(bk_tmp, tw1_, tw2_, bkf_, stream_), "bk_to_fft");
+    ++stats_.other_launches;
+    // the same key in the warp-FFT bin order of the v4 throughput kernel
+    if (!bkf4_) check(cudaMalloc(&bkf4_, kBkfBytes), "cudaMalloc(bkf4)");
+    check(launch_bk_to_fft_v4(bk_tmp, tw4_, bkf4_, stream_), "bk_to_fft_v4");
     ++stats_.other_launches;
     // KSK rows padded 631 -> 632 words (pad word zero)
     check(cudaMemsetAsync(ksk_, 0, ksk_rows * kKskRowStride * 4, stream_), "memset ksk");
@@ -273,7 +287,8 @@ class Context {
 
   void launch_level(const BrJob* d_br, uint64_t n_br, const KsJob* d_ks, uint64_t n_ks) {
     Prof* p = begin_prof(0);
-    check(launch_blind_rotate(d_br, int(n_br), slab_, bkf_, tw1_, tw2_, xlwe_, stream_),
+    check(launch_blind_rotate(d_br, int(n_br), slab_, bkf_, tw1_, tw2_, bkf4_, tw4_, xlwe_,
+                              stream_),
           "blind_rotate_kernel");
     end_prof(p);
     p = begin_prof(1);
@@ -507,6 +522,7 @@ class Context {
   int sm_count_ = 0;
   cudaStream_t stream_ = nullptr;
   c64 *tw1_ = nullptr, *tw2_ = nullptr, *bkf_ = nullptr;
+  c64 *tw4_ = nullptr, *bkf4_ = nullptr;  // warp-FFT twiddle bases and key (v4)
   uint32_t* ksk_ = nullptr;
   uint32_t* kskb_ = nullptr;   // KSK as byte limbs for the mma.sync key switch
   uint32_t* ksktc_ = nullptr;  // the same limbs as tcgen05 B tiles

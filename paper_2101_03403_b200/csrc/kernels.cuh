@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "fft512.cuh"
+#include "fft512w.cuh"
 #include "tfhe_params.h"
 
 namespace cvm {
@@ -32,15 +33,25 @@ struct KsJob {
 
 cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2, c64* bkf,
                              cudaStream_t s);
+// bkf4 / tw4: the key in the warp-FFT bin order and the per-lane twiddle
+// bases of the v4 kernels (blind_rotate_v4.cu, fft512w.cuh).
+cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, cudaStream_t s);
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
-                                uint32_t* xout, cudaStream_t s);
+                                const c64* bkf4, const c64* tw4, uint32_t* xout,
+                                cudaStream_t s);
+bool valid_br_v4_variant(int v);
+cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
+                                   const uint32_t* slab, const c64* bkf4, const c64* tw4,
+                                   uint32_t* xout, cudaStream_t s);
 // Blind-rotation kernel variant: 1 = v1 (one bootstrap per 64-thread CTA, key
 // via L1); 10*G + S = v2 (G bootstraps per CTA, S-stage bulk-copy key ring:
 // 13, 22, 23, 43); 3044 = v3 (G=4, S=4, two transforms per thread);
 // 4044 = v3 with the key ring in tensor memory (tcgen05.cp / tcgen05.ld);
 // 5044 / 5054 / 5063 = v3 G=4 / v3 G=5 / v2 G=6 with generated twiddles
 // (TwPow8; 5044 is the wide-level default);
+// 6000 + 100*(1 - hold) + 10*G + S = v4 (one bootstrap per warp, warp-wide
+// FFT, G warps per CTA on an S-row key ring: 6184, 6185, 6084, 6085);
 // 9 = wide latency kernel.  0 = auto by level width (default).  Env
 // CVM_BR_KERNEL overrides the default.
 constexpr int kDefaultBrVariant = 0;

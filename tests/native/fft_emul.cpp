@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "fft512.cuh"
+#include "fft512w.cuh"
 
 using namespace cvm;
 
@@ -157,6 +158,122 @@ static int run(int trials, bool rec, double* worst) {
   return 0;
 }
 
+// ------------------------------------------------ warp FFT (fft512w.cuh) --
+// 32 emulated lanes; the lane-pair swap of slots 8..15 stands in for the
+// kernel's shuffles.
+static void wswap(c64 v[32][16]) {
+  for (int l = 0; l < 32; l += 2)
+    for (int i = 8; i < 16; ++i) std::swap(v[l][i], v[l + 1][i]);
+}
+
+static void wforward(const double* p, c64 bins[32][16], bool key) {
+  c64 v[32][16];
+  c64 buf[512];
+  for (int t = 0; t < 32; ++t) {
+    for (int a = 0; a < 16; ++a) v[t][a] = {p[t + 32 * a], p[t + 32 * a + 512]};
+    wfwd_stage1(v[t], make_wbases(t));
+    for (int k0 = 0; k0 < 16; ++k0) buf[wpos(k0, t)] = v[t][k0];
+  }
+  for (int l = 0; l < 32; ++l) {
+    for (int s = 0; s < 16; ++s) v[l][s] = buf[wpos(l >> 1, wslot_t(l & 1, s))];
+    wfwd_stage2a(v[l], l & 1);
+  }
+  wswap(v);
+  for (int l = 0; l < 32; ++l) {
+    wfwd_stage2b(v[l]);
+    for (int r = 0; r < 16; ++r) {
+      c64 x = v[l][r];
+      if (key && (l & 1) && (r & 1)) x = {-x.x, -x.y};  // the key side stores F, not D F
+      bins[l][r] = x;
+    }
+  }
+}
+
+static void winverse(c64 bins[32][16], uint32_t* out, double* worst) {
+  c64 v[32][16];
+  c64 buf[512];
+  for (int l = 0; l < 32; ++l) {
+    for (int r = 0; r < 16; ++r) v[l][r] = bins[l][r];
+    winv_stage2b(v[l]);
+  }
+  wswap(v);
+  for (int l = 0; l < 32; ++l) {
+    winv_stage2a(v[l], l & 1);
+    for (int s = 0; s < 16; ++s) buf[wpos(l >> 1, wslot_t(l & 1, s))] = v[l][s];
+  }
+  for (int t = 0; t < 32; ++t) {
+    for (int k0 = 0; k0 < 16; ++k0) v[t][k0] = buf[wpos(k0, t)];
+    winv_stage1(v[t], make_wbases(t));
+    for (int a = 0; a < 16; ++a) {
+      for (double x : {v[t][a].x, v[t][a].y}) {
+        const double d = std::fabs(x - std::nearbyint(x));
+        if (d > *worst) *worst = d;
+      }
+      out[t + 32 * a] = round_to_torus(v[t][a].x);
+      out[t + 32 * a + 512] = round_to_torus(v[t][a].y);
+    }
+  }
+}
+
+static bool check_wswizzle() {
+  for (int q = 0; q < 4; ++q)
+    for (int z = 0; z < 16; ++z) {
+      int seen_w = 0, seen_r = 0;
+      for (int i = 0; i < 8; ++i) {
+        const int gw = wpos(z, 8 * q + i) & 7;                             // stage-1 write
+        const int l = 8 * q + i, gr = wpos(l >> 1, wslot_t(l & 1, z)) & 7;  // stage-2 read
+        if ((seen_w >> gw) & 1 || (seen_r >> gr) & 1) return false;
+        seen_w |= 1 << gw;
+        seen_r |= 1 << gr;
+      }
+    }
+  // the transpose is a bijection onto the 512 entries
+  int hit[512] = {};
+  for (int k0 = 0; k0 < 16; ++k0)
+    for (int t = 0; t < 32; ++t) ++hit[wpos(k0, t)];
+  for (int i = 0; i < 512; ++i)
+    if (hit[i] != 1) return false;
+  return true;
+}
+
+static int run_w(int trials, double* worst) {
+  std::mt19937_64 rng(11);
+  for (int trial = 0; trial < trials; ++trial) {
+    std::vector<uint32_t> exact(1024, 0);
+    c64 acc[32][16] = {};
+    for (int r = 0; r < 6; ++r) {
+      std::vector<int32_t> d(1024);
+      std::vector<uint32_t> b(1024);
+      for (auto& x : d) x = int32_t(rng() % 128) - 64;
+      for (auto& x : b) x = uint32_t(rng());
+      for (int i = 0; i < 1024; ++i)
+        for (int j = 0; j < 1024; ++j) {
+          uint32_t prod = uint32_t(d[i]) * b[j];
+          if (i + j < 1024) exact[i + j] += prod;
+          else exact[i + j - 1024] -= prod;
+        }
+      std::vector<double> dd(1024), bd(1024);
+      for (int i = 0; i < 1024; ++i) {
+        dd[i] = d[i];
+        bd[i] = double(int32_t(b[i])) / 512.0;
+      }
+      c64 D[32][16], B[32][16];
+      wforward(dd.data(), D, false);
+      wforward(bd.data(), B, true);
+      for (int l = 0; l < 32; ++l)
+        for (int k = 0; k < 16; ++k) acc[l][k] = cadd(acc[l][k], cmul(D[l][k], B[l][k]));
+    }
+    std::vector<uint32_t> got(1024);
+    winverse(acc, got.data(), worst);
+    for (int i = 0; i < 1024; ++i)
+      if (got[i] != exact[i]) {
+        printf("FAIL (warp) trial %d coef %d got %u want %u\n", trial, i, got[i], exact[i]);
+        return 1;
+      }
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   int trials = argc > 1 ? atoi(argv[1]) : 20;
   make_twiddles(T1, T2);
@@ -170,9 +287,14 @@ int main(int argc, char** argv) {
     printf("FAIL swizzle conflict\n");
     return 1;
   }
-  double worst_tab = 0, worst_rec = 0;
-  if (run(trials, false, &worst_tab) || run(trials, true, &worst_rec)) return 1;
+  if (!check_wswizzle()) {
+    printf("FAIL warp transpose conflict\n");
+    return 1;
+  }
+  double worst_tab = 0, worst_rec = 0, worst_w = 0;
+  if (run(trials, false, &worst_tab) || run(trials, true, &worst_rec) || run_w(trials, &worst_w))
+    return 1;
   printf("OK %d trials bit-exact (table twiddles: max distance to integer %.4g; "
-         "generated twiddles: %.4g)\n", trials, worst_tab, worst_rec);
+         "generated twiddles: %.4g; warp FFT: %.4g)\n", trials, worst_tab, worst_rec, worst_w);
   return 0;
 }

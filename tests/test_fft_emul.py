@@ -2,7 +2,9 @@
 __device__ functions) on the CPU with 64 emulated threads: exchange
 permutations, swizzle conflict-freedom and bit-exact negacyclic products,
 with the table twiddles and with the generated twiddles (TwPow8) of the
-default throughput kernel; the rounding margin of both is asserted."""
+v3 throughput kernel, and the warp-wide transform of the v4 kernel
+(csrc/fft512w.cuh: one transpose plus a lane-pair swap, 32 emulated lanes);
+the rounding margin of every mode is asserted."""
 import os
 import re
 import shutil
@@ -25,5 +27,6 @@ def test_fft_emulation_bit_exact(tmp_path):
     assert "bit-exact" in r.stdout
     tab, rec = (float(x) for x in re.findall(r"twiddles: (?:max distance to integer )?([0-9.e-]+)",
                                              r.stdout))
-    # a rounding flip needs 0.5; both modes keep a > 20x margin
-    assert tab < 0.025 and rec < 0.025, r.stdout
+    warp = float(re.search(r"warp FFT: ([0-9.e-]+)", r.stdout).group(1))
+    # a rounding flip needs 0.5; every mode keeps a > 20x margin
+    assert tab < 0.025 and rec < 0.025 and warp < 0.025, r.stdout
