@@ -949,13 +949,9 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
   if (variant == 0) {
     // auto: a very narrow level runs each bootstrap on a 2-SM cluster, a
     // narrow one on a whole SM (latency); a level of up to two bootstraps
-    // per SM gives each its own CTA; wide
-    // levels use the throughput kernel (v3 with generated twiddles, held
-    // rotated differences, a 7-row key ring refilled by each slot's last
-    // reader: 5247), whose SMs work in rounds of 4 bootstraps (~5.9 ms).  A
-    // last partial round of at most 2 bootstraps per SM is cheaper on the
-    // latency kernel (2 x 2.3 ms), so it is split off.
-    constexpr int kSms = 148, kRound = 4 * kSms;
+    // per SM gives each its own CTA; wide levels use the v4 throughput
+    // kernel (blind_rotate_v4.cu) with the remainder split off below.
+    constexpr int kSms = 148;
     if (count <= kSms / 2) {
       variant = 92;  // one bootstrap per 2-SM cluster: 1.62 vs 2.27 ms
     } else if (count <= kSms) {
@@ -963,14 +959,29 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     } else if (count <= 2 * kSms) {
       variant = 13;
     } else {
-      const int tail = count % kRound;
-      if (tail > 0 && tail <= 2 * kSms && count > kRound) {
-        cudaError_t e = launch_v3<4, 7, false, true, true, true>(jobs, count - tail, slab, bkf,
-                                                                 tw1, tw2, xout, s);
+      // Wide levels: the v4 kernel (one bootstrap per warp, 8 per SM) works
+      // in waves of 8 x 148 bootstraps (~11.3 ms), the v3 kernel (5247) in
+      // rounds of 4 x 148 (~5.8 ms), the latency kernel in rounds of 148
+      // (~2.3 ms).  Full v4 waves, then the remainder on whichever of the
+      // three finishes it first (costs in 0.1 ms, measured on C1-style
+      // levels: profiles/r01_variant_sweep.txt).
+      constexpr int kW8 = 8 * kSms, kW4 = 4 * kSms;
+      constexpr int kT8 = 113, kT4 = 58, kT1 = 23;
+      const int full = count / kW8, rest = count - full * kW8;
+      const int c8 = rest ? kT8 : 0;
+      const int c4 = (rest + kW4 - 1) / kW4 * kT4;
+      const int c1 = (rest + kSms - 1) / kSms * kT1;
+      const int head = full * kW8;
+      if (rest == 0 || (c8 <= c4 && c8 <= c1))
+        return launch_blind_rotate_v4(6085, jobs, count, slab, bkf4, tw4, xout, s);
+      if (head > 0) {
+        cudaError_t e = launch_blind_rotate_v4(6085, jobs, head, slab, bkf4, tw4, xout, s);
         if (e != cudaSuccess) return e;
-        return launch_wide(jobs + (count - tail), tail, slab, bkf, tw1, tw2, xout, s);
       }
-      variant = 5247;
+      if (c1 <= c4)
+        return launch_wide(jobs + head, rest, slab, bkf, tw1, tw2, xout, s);
+      return launch_v3<4, 7, false, true, true, true>(jobs + head, rest, slab, bkf, tw1, tw2,
+                                                       xout, s);
     }
   }
   switch (variant) {

@@ -85,9 +85,10 @@ __global__ void __launch_bounds__(32) bk_to_fft_v4_kernel(const uint32_t* __rest
 }
 
 // ---------------------------------------------------------- K1 + K2, v4 --
-template <int G, int S>
+template <int G, int S, bool kTab>
 struct BrSmem4 {
   c64 ring[S][1024];
+  c64 twt[kTab ? 512 : 1];  // kTab: stage-1 twiddles [k0][lane]
   c64 xbuf[G][512];
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
@@ -95,14 +96,18 @@ struct BrSmem4 {
   uint32_t cnt[S];  // warps done with each slot
 };
 
-// kHold: the 32 rotated-accumulator words of a part are kept in registers
-// across its three gadget levels instead of re-read per level.
-template <int G, int S, bool kHold>
+// kHold: the digits of gadget levels 1 and 2 of a part are kept in registers
+// (16 words, packed from the rotated differences read for level 0) instead
+// of re-reading the accumulator per level.
+// kTab: the 16 stage-1 twiddles of a lane come from a shared-memory table
+// (16 conflict-free LDS.128 per transform) instead of being generated from
+// two bases (18 complex multiplies per transform).
+template <int G, int S, bool kHold, bool kTab>
 __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf4, const c64* __restrict__ tw4, uint32_t* __restrict__ xout) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  BrSmem4<G, S>& sm = *reinterpret_cast<BrSmem4<G, S>*>(smem_raw);
+  BrSmem4<G, S, kTab>& sm = *reinterpret_cast<BrSmem4<G, S, kTab>*>(smem_raw);
   const int tid = threadIdx.x;
   const int g = tid >> 5, l = tid & 31, e = l & 1;
   const int jidx = blockIdx.x * G + g;
@@ -123,6 +128,10 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
       mbar_expect_tx(&sm.full[q], kRowBytes);
       bulk_g2s(sm.ring[q], bkf4 + (size_t)q * 1024, kRowBytes, &sm.full[q]);
     }
+  }
+  if constexpr (kTab) {
+    for (int x = tid; x < 512; x += 32 * G) sm.twt[x] = ldg_c64(tw4 + 64 + x);
+    __syncthreads();
   }
   const TwBasesW tb = load_wbases(tw4, l);
   uint32_t* acc0 = sm.acc[g][0];
@@ -152,29 +161,39 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
         d0 = r0 - accp[j] + kDecompOffset;
         d1 = r1 - accp[j + 512] + kDecompOffset;
       };
-      uint32_t dh[kHold ? 16 : 1][2];
-      if constexpr (kHold) {
-#pragma unroll
-        for (int a = 0; a < 16; ++a) rdiff(a, dh[a][0], dh[a][1]);
-      }
+      // kHold: level 0 reads the rotated differences and keeps the bits of
+      // levels 1 and 2 (bits kLow .. kLow+13), two coefficients per register
+      constexpr int kLow = 32 - kL * kBgBit;
+      uint32_t pk[kHold ? 16 : 1];
 #pragma unroll 1
       for (int p = 0; p < kL; ++p, ++q) {
         const int shift = 32 - (p + 1) * kBgBit;
         c64 v[16];
+        if (!kHold || p == 0) {
 #pragma unroll
-        for (int a = 0; a < 16; ++a) {
-          uint32_t d0, d1;
-          if constexpr (kHold) {
-            d0 = dh[a][0];
-            d1 = dh[a][1];
-          } else {
+          for (int a = 0; a < 16; ++a) {
+            uint32_t d0, d1;
             rdiff(a, d0, d1);
+            if constexpr (kHold)
+              pk[a] = ((d0 >> kLow) & 0x3FFFu) | (((d1 >> kLow) & 0x3FFFu) << 16);
+            v[a] = {u32_biased_to_double((d0 >> shift) & 127u, kDigitBias),
+                    u32_biased_to_double((d1 >> shift) & 127u, kDigitBias)};
           }
-          v[a] = {u32_biased_to_double((d0 >> shift) & 127u, kDigitBias),
-                  u32_biased_to_double((d1 >> shift) & 127u, kDigitBias)};
+        } else {
+          const int sh = shift - kLow;
+#pragma unroll
+          for (int a = 0; a < 16; ++a)
+            v[a] = {u32_biased_to_double((pk[a] >> sh) & 127u, kDigitBias),
+                    u32_biased_to_double((pk[a] >> (16 + sh)) & 127u, kDigitBias)};
         }
-        wfwd_stage1(v, opaque(tb));
         const int lo = opaque(l), eo = lo & 1;
+        if constexpr (kTab) {
+          wfwd_twist_dft(v);
+#pragma unroll
+          for (int k0 = 0; k0 < 16; ++k0) v[k0] = cmul(v[k0], sm.twt[k0 * 32 + lo]);
+        } else {
+          wfwd_stage1(v, opaque(tb));
+        }
 #pragma unroll
         for (int k0 = 0; k0 < 16; ++k0) xb[wpos(k0, lo)] = v[k0];
         __syncwarp();
@@ -223,7 +242,13 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) v[k0] = xb[wpos(k0, lo)];
       __syncwarp();
-      winv_stage1(v, opaque(tb));
+      if constexpr (kTab) {
+#pragma unroll
+        for (int k0 = 0; k0 < 16; ++k0) v[k0] = cmul_conj(v[k0], sm.twt[k0 * 32 + lo]);
+        winv_dft_untwist(v);
+      } else {
+        winv_stage1(v, opaque(tb));
+      }
       uint32_t* accp = o ? acc1 : acc0;
 #pragma unroll
       for (int a = 0; a < 16; ++a) {
@@ -242,19 +267,21 @@ cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, c
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kHold>
+template <int G, int S, bool kHold, bool kTab = false>
 static cudaError_t launch_v4(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf4,
                              const c64* tw4, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
-  const int smem = int(sizeof(BrSmem4<G, S>));
-  auto* kern = blind_rotate_kernel_v4<G, S, kHold>;
+  const int smem = int(sizeof(BrSmem4<G, S, kTab>));
+  auto* kern = blind_rotate_kernel_v4<G, S, kHold, kTab>;
   cudaError_t e = set_smem(kern, smem, configured);
   if (e != cudaSuccess) return e;
   kern<<<(count + G - 1) / G, 32 * G, smem, s>>>(jobs, count, slab, bkf4, tw4, xout);
   return cudaGetLastError();
 }
 
-bool valid_br_v4_variant(int v) { return v == 6085 || v == 6084 || v == 6185 || v == 6184; }
+bool valid_br_v4_variant(int v) {
+  return v == 6085 || v == 6084 || v == 6185 || v == 6184 || v == 6284 || v == 6384;
+}
 
 cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
                                    const uint32_t* slab, const c64* bkf4, const c64* tw4,
@@ -264,6 +291,8 @@ cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
     case 6084: return launch_v4<8, 4, true>(jobs, count, slab, bkf4, tw4, xout, s);
     case 6185: return launch_v4<8, 5, false>(jobs, count, slab, bkf4, tw4, xout, s);
     case 6184: return launch_v4<8, 4, false>(jobs, count, slab, bkf4, tw4, xout, s);
+    case 6284: return launch_v4<8, 4, true, true>(jobs, count, slab, bkf4, tw4, xout, s);
+    case 6384: return launch_v4<8, 4, false, true>(jobs, count, slab, bkf4, tw4, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -160,10 +160,13 @@ struct TwBasesW {
 
 // ---------------------------------------------------------------- forward --
 // Input v[a] = p_{t+32a} + i p_{t+32a+512} (untwisted).
-CVM_HD void wfwd_stage1(c64 v[16], const TwBasesW& b) {
+CVM_HD void wfwd_twist_dft(c64 v[16]) {
 #pragma unroll
   for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], twist32(a));
   dft16<false>(v);
+}
+CVM_HD void wfwd_stage1(c64 v[16], const TwBasesW& b) {
+  wfwd_twist_dft(v);
   apply_pow16<false>(v, b.base, b.w);
 }
 
@@ -216,11 +219,14 @@ CVM_HD void winv_stage2a(c64 v[16], int e) {
     v[8 + i] = csub(s, c);
   }
 }
-CVM_HD void winv_stage1(c64 v[16], const TwBasesW& b) {
-  apply_pow16<true>(v, b.base, b.w);
+CVM_HD void winv_dft_untwist(c64 v[16]) {
   dft16<true>(v);
 #pragma unroll
   for (int a = 1; a < 16; ++a) v[a] = cmul_conj(v[a], twist32(a));
+}
+CVM_HD void winv_stage1(c64 v[16], const TwBasesW& b) {
+  apply_pow16<true>(v, b.base, b.w);
+  winv_dft_untwist(v);
 }
 
 // Host-side exact bases for lane t (long double), shared by the device
@@ -229,6 +235,17 @@ inline TwBasesW make_wbases(int t) {
   const long double pi = 3.141592653589793238462643383279502884L;
   const long double ab = pi * t / 1024.0L, aw = -pi * 4 * t / 1024.0L;
   return {{(double)std::cos(ab), (double)std::sin(ab)}, {(double)std::cos(aw), (double)std::sin(aw)}};
+}
+
+// Host-side exact stage-1 twiddle table, T[k0][t] = e^{i pi t (1 - 4 k0) / 1024}
+// (the table mode of the v4 kernel keeps it in shared memory).
+inline void make_wtable(c64 T[16][32]) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int k0 = 0; k0 < 16; ++k0)
+    for (int t = 0; t < 32; ++t) {
+      const long double a = pi * t * (1 - 4 * k0) / 1024.0L;
+      T[k0][t] = {(double)std::cos(a), (double)std::sin(a)};
+    }
 }
 
 }  // namespace cvm
