@@ -960,11 +960,12 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       variant = 13;
     } else {
       // Wide levels: the v4 kernel (one bootstrap per warp, 8 per SM) works
-      // in waves of 8 x 148 bootstraps (~11.3 ms), the v3 kernel (5247) in
-      // rounds of 4 x 148 (~5.8 ms), the latency kernel in rounds of 148
-      // (~2.3 ms).  Full v4 waves, then the remainder on whichever of the
-      // three finishes it first (costs in 0.1 ms, measured on C1-style
-      // levels: profiles/r01_variant_sweep.txt).
+      // in waves of 8 x 148 bootstraps (~11.4 ms; with 5-7 warps per SM a
+      // wave still takes ~11.2 ms, with 2-4 ~8.1 ms: a lone warp is
+      // latency-bound), the v3 kernel (5247) in rounds of 4 x 148 (~5.9 ms),
+      // the latency kernel in rounds of 148 (~2.3 ms).  Full v4 waves, then
+      // the remainder on whichever finishes it first (costs in 0.1 ms,
+      // tools/v4_waves.py; profiles/r01_variant_sweep.txt).
       constexpr int kW8 = 8 * kSms, kW4 = 4 * kSms;
       constexpr int kT8 = 113, kT4 = 58, kT1 = 23;
       const int full = count / kW8, rest = count - full * kW8;
@@ -972,11 +973,14 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       const int c4 = (rest + kW4 - 1) / kW4 * kT4;
       const int c1 = (rest + kSms - 1) / kSms * kT1;
       const int head = full * kW8;
-      if (rest == 0 || (c8 <= c4 && c8 <= c1))
-        return launch_blind_rotate_v4(6085, jobs, count, slab, bkf4, tw4, xout, s);
       if (head > 0) {
         cudaError_t e = launch_blind_rotate_v4(6085, jobs, head, slab, bkf4, tw4, xout, s);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess || rest == 0) return e;
+      }
+      if (c8 <= c4 && c8 <= c1) {  // one more v4 wave, rest/148 warps per SM
+        const int warps = (rest + kSms - 1) / kSms;
+        return launch_blind_rotate_v4(6005 + 10 * warps, jobs + head, rest, slab, bkf4, tw4,
+                                      xout, s);
       }
       if (c1 <= c4)
         return launch_wide(jobs + head, rest, slab, bkf, tw1, tw2, xout, s);

@@ -18,6 +18,8 @@
 // conflict-free LDS.128.
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 #include "br_common.cuh"
 #include "fft512w.cuh"
 #include "kernels.cuh"
@@ -85,32 +87,40 @@ __global__ void __launch_bounds__(32) bk_to_fft_v4_kernel(const uint32_t* __rest
 }
 
 // ---------------------------------------------------------- K1 + K2, v4 --
-template <int G, int S, bool kTab>
+// Per-bootstrap (per-warp) shared memory.
+struct WarpSmem4 {
+  c64 xbuf[512];                // the transpose buffer
+  uint32_t acc[2][kPolyN];      // ACC (both TRLWE parts)
+  uint16_t bar[kLweWords + 1];  // mod-switched input sample
+};
+constexpr int kV4MaxWarps = 8;
+template <int S>
 struct BrSmem4 {
-  c64 ring[S][1024];
-  c64 twt[kTab ? 512 : 1];  // kTab: stage-1 twiddles [k0][lane]
-  c64 xbuf[G][512];
-  uint32_t acc[G][2][kPolyN];
-  uint16_t bar[G][kLweWords + 1];
   uint64_t full[S];
   uint32_t cnt[S];  // warps done with each slot
+  alignas(128) c64 ring[S][1024];
+  WarpSmem4 w[kV4MaxWarps];  // only blockDim.x / 32 of them are allocated
 };
+template <int S>
+constexpr int v4_smem_bytes(int warps) {
+  return int(offsetof(BrSmem4<S>, w) + sizeof(WarpSmem4) * warps);
+}
 
+// One CTA of blockDim.x / 32 <= 8 warps (runtime: a partial last wave runs
+// with fewer bootstraps per SM instead of idle SMs), one bootstrap per warp.
 // kHold: the digits of gadget levels 1 and 2 of a part are kept in registers
 // (16 words, packed from the rotated differences read for level 0) instead
 // of re-reading the accumulator per level.
-// kTab: the 16 stage-1 twiddles of a lane come from a shared-memory table
-// (16 conflict-free LDS.128 per transform) instead of being generated from
-// two bases (18 complex multiplies per transform).
-template <int G, int S, bool kHold, bool kTab>
-__global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
+template <int S, bool kHold>
+__global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf4, const c64* __restrict__ tw4, uint32_t* __restrict__ xout) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  BrSmem4<G, S, kTab>& sm = *reinterpret_cast<BrSmem4<G, S, kTab>*>(smem_raw);
+  BrSmem4<S>& sm = *reinterpret_cast<BrSmem4<S>*>(smem_raw);
   const int tid = threadIdx.x;
+  const int nw = blockDim.x >> 5;
   const int g = tid >> 5, l = tid & 31, e = l & 1;
-  const int jidx = blockIdx.x * G + g;
+  const int jidx = blockIdx.x * nw + g;
   const bool live = jidx < count;
   const BrJob job = jobs[live ? jidx : 0];
   constexpr int kChunks = kN * kRows;
@@ -129,15 +139,11 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
       bulk_g2s(sm.ring[q], bkf4 + (size_t)q * 1024, kRowBytes, &sm.full[q]);
     }
   }
-  if constexpr (kTab) {
-    for (int x = tid; x < 512; x += 32 * G) sm.twt[x] = ldg_c64(tw4 + 64 + x);
-    __syncthreads();
-  }
   const TwBasesW tb = load_wbases(tw4, l);
-  uint32_t* acc0 = sm.acc[g][0];
-  uint32_t* acc1 = sm.acc[g][1];
-  uint16_t* bar = sm.bar[g];
-  c64* xb = sm.xbuf[g];
+  uint32_t* acc0 = sm.w[g].acc[0];
+  uint32_t* acc1 = sm.w[g].acc[1];
+  uint16_t* bar = sm.w[g].bar;
+  c64* xb = sm.w[g].xbuf;
   prologue(job, slab, bar, acc0, acc1, l, 32, warp_sync, 0);
 
   int q = 0;
@@ -187,13 +193,7 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
                     u32_biased_to_double((pk[a] >> (16 + sh)) & 127u, kDigitBias)};
         }
         const int lo = opaque(l), eo = lo & 1;
-        if constexpr (kTab) {
-          wfwd_twist_dft(v);
-#pragma unroll
-          for (int k0 = 0; k0 < 16; ++k0) v[k0] = cmul(v[k0], sm.twt[k0 * 32 + lo]);
-        } else {
-          wfwd_stage1(v, opaque(tb));
-        }
+        wfwd_stage1(v, opaque(tb));
 #pragma unroll
         for (int k0 = 0; k0 < 16; ++k0) xb[wpos(k0, lo)] = v[k0];
         __syncwarp();
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
         __syncwarp();
         if (l == 0) {
           __threadfence_block();
-          if (atomicAdd(&sm.cnt[slot], 1u) == unsigned(G - 1)) {
+          if (atomicAdd(&sm.cnt[slot], 1u) == unsigned(nw - 1)) {
             sm.cnt[slot] = 0;
             if (q + S < kChunks) {
               mbar_expect_tx(&sm.full[slot], kRowBytes);
@@ -242,13 +242,7 @@ __global__ void __launch_bounds__(32 * G, 1) blind_rotate_kernel_v4(
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) v[k0] = xb[wpos(k0, lo)];
       __syncwarp();
-      if constexpr (kTab) {
-#pragma unroll
-        for (int k0 = 0; k0 < 16; ++k0) v[k0] = cmul_conj(v[k0], sm.twt[k0 * 32 + lo]);
-        winv_dft_untwist(v);
-      } else {
-        winv_stage1(v, opaque(tb));
-      }
+      winv_stage1(v, opaque(tb));
       uint32_t* accp = o ? acc1 : acc0;
 #pragma unroll
       for (int a = 0; a < 16; ++a) {
@@ -267,34 +261,35 @@ cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, c
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kHold, bool kTab = false>
-static cudaError_t launch_v4(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf4,
-                             const c64* tw4, uint32_t* xout, cudaStream_t s) {
+template <int S, bool kHold>
+static cudaError_t launch_v4(int warps, const BrJob* jobs, int count, const uint32_t* slab,
+                             const c64* bkf4, const c64* tw4, uint32_t* xout, cudaStream_t s) {
   static bool configured = false;
-  const int smem = int(sizeof(BrSmem4<G, S, kTab>));
-  auto* kern = blind_rotate_kernel_v4<G, S, kHold, kTab>;
-  cudaError_t e = set_smem(kern, smem, configured);
+  auto* kern = blind_rotate_kernel_v4<S, kHold>;
+  cudaError_t e = set_smem(kern, v4_smem_bytes<S>(kV4MaxWarps), configured);
   if (e != cudaSuccess) return e;
-  kern<<<(count + G - 1) / G, 32 * G, smem, s>>>(jobs, count, slab, bkf4, tw4, xout);
+  kern<<<(count + warps - 1) / warps, 32 * warps, v4_smem_bytes<S>(warps), s>>>(
+      jobs, count, slab, bkf4, tw4, xout);
   return cudaGetLastError();
 }
 
+// 6000 + 100 * (1 - hold) + 10 * warps + S, warps = 1..8, S = 4 or 5
 bool valid_br_v4_variant(int v) {
-  return v == 6085 || v == 6084 || v == 6185 || v == 6184 || v == 6284 || v == 6384;
+  const int h = (v / 100) % 10, w = (v / 10) % 10, st = v % 10;
+  return v / 1000 == 6 && h <= 1 && w >= 1 && w <= kV4MaxWarps && (st == 4 || st == 5);
 }
 
 cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
                                    const uint32_t* slab, const c64* bkf4, const c64* tw4,
                                    uint32_t* xout, cudaStream_t s) {
-  switch (variant) {
-    case 6085: return launch_v4<8, 5, true>(jobs, count, slab, bkf4, tw4, xout, s);
-    case 6084: return launch_v4<8, 4, true>(jobs, count, slab, bkf4, tw4, xout, s);
-    case 6185: return launch_v4<8, 5, false>(jobs, count, slab, bkf4, tw4, xout, s);
-    case 6184: return launch_v4<8, 4, false>(jobs, count, slab, bkf4, tw4, xout, s);
-    case 6284: return launch_v4<8, 4, true, true>(jobs, count, slab, bkf4, tw4, xout, s);
-    case 6384: return launch_v4<8, 4, false, true>(jobs, count, slab, bkf4, tw4, xout, s);
-    default: return cudaErrorInvalidValue;
-  }
+  if (!valid_br_v4_variant(variant)) return cudaErrorInvalidValue;
+  const bool hold = (variant / 100) % 10 == 0;
+  const int warps = (variant / 10) % 10, st = variant % 10;
+  if (hold)
+    return st == 5 ? launch_v4<5, true>(warps, jobs, count, slab, bkf4, tw4, xout, s)
+                   : launch_v4<4, true>(warps, jobs, count, slab, bkf4, tw4, xout, s);
+  return st == 5 ? launch_v4<5, false>(warps, jobs, count, slab, bkf4, tw4, xout, s)
+                 : launch_v4<4, false>(warps, jobs, count, slab, bkf4, tw4, xout, s);
 }
 
 }  // namespace cvm

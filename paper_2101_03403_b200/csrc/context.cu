@@ -86,15 +86,12 @@ class Context {
     check(cudaMalloc(&tw2_, sizeof(T2)), "cudaMalloc(tw2)");
     check(cudaMemcpy(tw1_, T1, sizeof(T1), cudaMemcpyHostToDevice), "tw1");
     check(cudaMemcpy(tw2_, T2, sizeof(T2), cudaMemcpyHostToDevice), "tw2");
-    // warp FFT (v4): per-lane twiddle bases [32][2], then the stage-1 table
-    // [16][32] of the table mode
-    c64 T4[64 + 512];
+    c64 T4[64];  // warp FFT (v4): per-lane twiddle bases [32][2]
     for (int l = 0; l < 32; ++l) {
       const TwBasesW b = make_wbases(l);
       T4[2 * l] = b.base;
       T4[2 * l + 1] = b.w;
     }
-    make_wtable(reinterpret_cast<c64(*)[32]>(T4 + 64));
     check(cudaMalloc(&tw4_, sizeof(T4)), "cudaMalloc(tw4)");
     check(cudaMemcpy(tw4_, T4, sizeof(T4), cudaMemcpyHostToDevice), "tw4");
     check(cudaEventCreate(&ev_user_[0]), "event");

@@ -237,15 +237,4 @@ inline TwBasesW make_wbases(int t) {
   return {{(double)std::cos(ab), (double)std::sin(ab)}, {(double)std::cos(aw), (double)std::sin(aw)}};
 }
 
-// Host-side exact stage-1 twiddle table, T[k0][t] = e^{i pi t (1 - 4 k0) / 1024}
-// (the table mode of the v4 kernel keeps it in shared memory).
-inline void make_wtable(c64 T[16][32]) {
-  const long double pi = 3.141592653589793238462643383279502884L;
-  for (int k0 = 0; k0 < 16; ++k0)
-    for (int t = 0; t < 32; ++t) {
-      const long double a = pi * t * (1 - 4 * k0) / 1024.0L;
-      T[k0][t] = {(double)std::cos(a), (double)std::sin(a)};
-    }
-}
-
 }  // namespace cvm
