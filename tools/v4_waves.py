@@ -19,13 +19,15 @@ def main():
     ctx.upload_keyset(ks)
     ctx.set_profiling(True)
     rng = np.random.default_rng(0)
-    nmax = 148 * 8
+    nmax = 148 * 12
     a, b = rng.integers(0, 2, nmax), rng.integers(0, 2, nmax)
     base = ctx.alloc(3 * nmax)
     ctx.upload(base, ks.encrypt(a, 1))
     ctx.upload(base + nmax, ks.encrypt(b, 2))
     plan = [(6000 + 10 * w + 5, 148 * w) for w in range(1, 9)]
     plan += [(5247, 148 * 4), (5247, 148 * 2), (9, 148), (13, 296)]
+    if os.environ.get("PLAN"):  # "variant:count,..."
+        plan = [tuple(int(x) for x in it.split(":")) for it in os.environ["PLAN"].split(",")]
     res = {}
     for v, n in plan:
         gates = [("NAND", [(base + i, 1, 0), (base + nmax + i, 1, 0)], base + 2 * nmax + i)
