@@ -436,7 +436,8 @@ def run_ours(args):
     prof = os.path.join(REPO, "profiles", "ncu_blind_rotate.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof))["blind_rotate_v3"]["avg_dram_bytes_per_launch"]
+            pj = json.load(open(prof))
+            traffic = pj[pj.get("dominant", "blind_rotate_v3")]["avg_dram_bytes_per_launch"]
         except (KeyError, ValueError):
             traffic = None
     line = {
@@ -457,7 +458,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(BATCH * (WIDTH + 1) * 631 * 4),
                 "gates_executed_per_step": e2e_gates * ws,
                 "add16_ops_per_s": e2e_add16},
-        "roofline": {"bound": "fp64", "kernel": "blind_rotate_kernel",
+        "roofline": {"bound": "fp64", "kernel": "blind_rotate_kernel_v4 (+ v3/wide remainders)",
                      "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per blind_rotate launch (ncu)",

@@ -969,23 +969,39 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       constexpr int kW8 = 8 * kSms, kW4 = 4 * kSms;
       constexpr int kT8 = 113, kT4 = 58, kT1 = 23;
       const int full = count / kW8, rest = count - full * kW8;
-      const int c8 = rest ? kT8 : 0;
-      const int c4 = (rest + kW4 - 1) / kW4 * kT4;
-      const int c1 = (rest + kSms - 1) / kSms * kT1;
       const int head = full * kW8;
       if (head > 0) {
         cudaError_t e = launch_blind_rotate_v4(6085, jobs, head, slab, bkf4, tw4, xout, s);
         if (e != cudaSuccess || rest == 0) return e;
       }
-      if (c8 <= c4 && c8 <= c1) {  // one more v4 wave, rest/148 warps per SM
-        const int warps = (rest + kSms - 1) / kSms;
-        return launch_blind_rotate_v4(6005 + 10 * warps, jobs + head, rest, slab, bkf4, tw4,
-                                      xout, s);
+      // the remainder: at most one more v4 wave, two v3 rounds and four
+      // latency rounds, the cheapest combination that covers it
+      int best = 1 << 30, b8 = 0, b4 = 0, b1 = 0;
+      for (int n8 = 0; n8 <= 1; ++n8)
+        for (int n4 = 0; n4 <= 2; ++n4)
+          for (int n1 = 0; n1 <= 4; ++n1) {
+            if (n8 * kW8 + n4 * kW4 + n1 * kSms < rest) continue;
+            const int c = n8 * kT8 + n4 * kT4 + n1 * kT1;
+            if (c < best) best = c, b8 = n8, b4 = n4, b1 = n1;
+          }
+      int done = head;
+      if (b8) {  // rest/148 warps per SM
+        const int n = std::min(rest, kW8), warps = (n + kSms - 1) / kSms;
+        cudaError_t e = launch_blind_rotate_v4(6005 + 10 * warps, jobs + done, n, slab, bkf4,
+                                               tw4, xout, s);
+        if (e != cudaSuccess) return e;
+        done += n;
       }
-      if (c1 <= c4)
-        return launch_wide(jobs + head, rest, slab, bkf, tw1, tw2, xout, s);
-      return launch_v3<4, 7, false, true, true, true>(jobs + head, rest, slab, bkf, tw1, tw2,
-                                                       xout, s);
+      if (b4 && done < count) {
+        const int n = std::min(count - done, b4 * kW4);
+        cudaError_t e = launch_v3<4, 7, false, true, true, true>(jobs + done, n, slab, bkf, tw1,
+                                                                 tw2, xout, s);
+        if (e != cudaSuccess) return e;
+        done += n;
+      }
+      if (b1 && done < count) return launch_wide(jobs + done, count - done, slab, bkf, tw1, tw2,
+                                                  xout, s);
+      return cudaSuccess;
     }
   }
   switch (variant) {
