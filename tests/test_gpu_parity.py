@@ -74,6 +74,35 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
+@pytest.mark.parametrize("n", [700, 1224, 1584, 1984])
+def test_wide_level_planner_bit_identical(n, keyset, ctx):
+    """Auto selection of a wide level: full waves of the v4 warp kernel, then
+    the remainder on another v4 wave with fewer warps per SM, on v3 rounds
+    and/or latency rounds (blind_rotate.cu).  The sizes hit each combination;
+    the result must equal the whole level on one kernel (6085, pinned to the
+    oracle by test_kernel_variants_bit_identical)."""
+    from paper_2101_03403_b200._native import lib, check
+    a, b = _bits(n, 40), _bits(n, 41)
+    ca, cb = keyset.encrypt(a, 81), keyset.encrypt(b, 82)
+    base = ctx.alloc(4 * n)
+    ctx.upload(base, ca)
+    ctx.upload(base + n, cb)
+    gates = lambda dst: [("AND", [(base + i, 1, 0), (base + n + i, 1, 0)], dst + i)  # noqa: E731
+                         for i in range(n)]
+    old = lib.cvm_get_br_variant()
+    try:
+        check(lib.cvm_set_br_variant(0))
+        ctx.submit_level(gates(base + 2 * n))
+        check(lib.cvm_set_br_variant(6085))
+        ctx.submit_level(gates(base + 3 * n))
+        ctx.sync()
+    finally:
+        check(lib.cvm_set_br_variant(old))
+    auto, ref = ctx.download(base + 2 * n, n), ctx.download(base + 3 * n, n)
+    assert np.array_equal(auto, ref)
+    assert np.array_equal(keyset.decrypt(auto), a & b)
+
+
 @pytest.mark.parametrize("ks_variant", [1, 6, 7, 8])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
