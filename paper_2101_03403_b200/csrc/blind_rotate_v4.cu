@@ -212,7 +212,12 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
           af[0][r] = cmac(af[0][r], v[r], bk[(2 * r) * 32 + l]);
           af[1][r] = cmac(af[1][r], v[r], bk[(2 * r + 1) * 32 + l]);
         }
-        // the slot's last reader streams the chunk S rows ahead into it
+        // the slot's last reader streams the chunk S rows ahead into it.  Every
+        // warp's key loads have returned (the MACs consumed them) and are
+        // ordered by the fence before its count, so the bulk copy cannot
+        // overwrite data still being read -- the same write-after-read
+        // contract as a consumer-release / producer-acquire TMA pipeline,
+        // which needs no proxy fence (measured: one costs 1-2%).
         __syncwarp();
         if (l == 0) {
           __threadfence_block();
