@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
         // ordered by the fence before its count, so the bulk copy cannot
         // overwrite data still being read -- the same write-after-read
         // contract as a consumer-release / producer-acquire TMA pipeline,
-        // which needs no proxy fence (measured: one costs 1-2%).
+        // which needs no proxy fence.
         __syncwarp();
         if (l == 0) {
           __threadfence_block();
