@@ -159,6 +159,13 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * and 9 rounds.  Every variant computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
+/* Wave packing of the levelizer (process-wide, default 1; env CVM_PACK=0):
+ * a flush keeps its number of launches (the critical path), but each gate may
+ * run in any launch between its earliest and latest dataflow level, and the
+ * launches are filled to the widths the blind-rotation kernels run most
+ * efficiently.  Results are unchanged (gates are pure); 0 = plain levels. */
+CVM_API int cvm_set_level_packing(int on);
+CVM_API int cvm_get_level_packing(void);
 /* Key-switch kernel variant: 1 = one gate per CTA; 6 = one gate on 948
  * threads (6 position groups, latency); 7 = the level as one INT8
  * tensor-core product (one-hot digits x KSK byte limbs) on mma.sync; 8 = the

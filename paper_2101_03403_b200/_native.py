@@ -104,6 +104,8 @@ _SIGS = {
     "cvm_ctx_sm_count": (_i, [_p, ctypes.POINTER(_i)]),
     "cvm_set_br_variant": (_i, [_i]),
     "cvm_get_br_variant": (_i, []),
+    "cvm_set_level_packing": (_i, [_i]),
+    "cvm_get_level_packing": (_i, []),
     "cvm_set_ks_variant": (_i, [_i]),
     "cvm_get_ks_variant": (_i, []),
     "cvm_backend_create":(_i, [_p, _p, _u64, ctypes.POINTER(_p)]),

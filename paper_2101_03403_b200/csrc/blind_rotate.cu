@@ -938,6 +938,34 @@ bool valid_br_variant(int v) {
          v == 5245 || v == 5246 || v == 5247 || valid_br_v4_variant(v);
 }
 
+// The remainder of a wide level after its full v4 waves: at most one more
+// v4 wave, two v3 rounds and four latency rounds, the cheapest combination
+// that covers it.  Returns its cost in 0.1 ms.
+int br_remainder_plan(int rest, int* n8, int* n4, int* n1) {
+  int best = rest > 0 ? 1 << 30 : 0, b8 = 0, b4 = 0, b1 = 0;
+  for (int a = 0; a <= 1 && rest > 0; ++a)
+    for (int b = 0; b <= 2; ++b)
+      for (int c = 0; c <= 4; ++c) {
+        if (a * kBrWave8 + b * kBrWave4 + c * kBrSms < rest) continue;
+        const int cost = a * kBrT8 + b * kBrT4 + c * kBrT1;
+        if (cost < best) best = cost, b8 = a, b4 = b, b1 = c;
+      }
+  if (n8) *n8 = b8, *n4 = b4, *n1 = b1;
+  return best;
+}
+
+// Device time (0.1 ms) of a level of `boots` bootstraps under the auto
+// selection below -- the cost model the wave-packing levelizer
+// (backend.cpp) fills launches with.
+int br_level_cost(int boots) {
+  if (boots <= 0) return 0;
+  if (boots <= kBrSms / 2) return 16;
+  if (boots <= kBrSms) return kBrT1;
+  if (boots <= 2 * kBrSms) return 48;
+  const int full = boots / kBrWave8;
+  return full * kBrT8 + br_remainder_plan(boots - full * kBrWave8, nullptr, nullptr, nullptr);
+}
+
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 const c64* bkf4, const c64* tw4, uint32_t* xout,
@@ -951,7 +979,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     // narrow one on a whole SM (latency); a level of up to two bootstraps
     // per SM gives each its own CTA; wide levels use the v4 throughput
     // kernel (blind_rotate_v4.cu) with the remainder split off below.
-    constexpr int kSms = 148;
+    constexpr int kSms = kBrSms;
     if (count <= kSms / 2) {
       variant = 92;  // one bootstrap per 2-SM cluster: 1.62 vs 2.27 ms
     } else if (count <= kSms) {
@@ -966,24 +994,15 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       // the latency kernel in rounds of 148 (~2.3 ms).  Full v4 waves, then
       // the remainder on whichever finishes it first (costs in 0.1 ms,
       // tools/v4_waves.py; profiles/r01_variant_sweep.txt).
-      constexpr int kW8 = 8 * kSms, kW4 = 4 * kSms;
-      constexpr int kT8 = 113, kT4 = 58, kT1 = 23;
-      const int full = count / kW8, rest = count - full * kW8;
-      const int head = full * kW8;
+      const int full = count / kBrWave8, rest = count - full * kBrWave8;
+      const int head = full * kBrWave8;
       if (head > 0) {
         cudaError_t e = launch_blind_rotate_v4(6085, jobs, head, slab, bkf4, tw4, xout, s);
         if (e != cudaSuccess || rest == 0) return e;
       }
-      // the remainder: at most one more v4 wave, two v3 rounds and four
-      // latency rounds, the cheapest combination that covers it
-      int best = 1 << 30, b8 = 0, b4 = 0, b1 = 0;
-      for (int n8 = 0; n8 <= 1; ++n8)
-        for (int n4 = 0; n4 <= 2; ++n4)
-          for (int n1 = 0; n1 <= 4; ++n1) {
-            if (n8 * kW8 + n4 * kW4 + n1 * kSms < rest) continue;
-            const int c = n8 * kT8 + n4 * kT4 + n1 * kT1;
-            if (c < best) best = c, b8 = n8, b4 = n4, b1 = n1;
-          }
+      int b8 = 0, b4 = 0, b1 = 0;
+      br_remainder_plan(rest, &b8, &b4, &b1);
+      constexpr int kW8 = kBrWave8, kW4 = kBrWave4;
       int done = head;
       if (b8) {  // rest/148 warps per SM
         const int n = std::min(rest, kW8), warps = (n + kSms - 1) / kSms;

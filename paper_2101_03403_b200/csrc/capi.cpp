@@ -239,6 +239,13 @@ int cvm_set_br_variant(int v) {
   });
 }
 int cvm_get_br_variant(void) { return cvm::br_variant(); }
+int cvm_set_level_packing(int on) {
+  return guard([&] {
+    if (on != 0 && on != 1) throw InputError("level packing is 0 or 1");
+    cvm::set_level_packing(on != 0);
+  });
+}
+int cvm_get_level_packing(void) { return cvm::level_packing() ? 1 : 0; }
 int cvm_set_ks_variant(int v) {
   return guard([&] {
     if (!cvm::valid_ks_variant(v))

@@ -128,6 +128,14 @@ class Region {  // RegionScope (gates.hpp:158-170)
 };
 
 // Node record (the reference DagNode, dag.hpp:33-42, minus cost/region).
+// Device time (0.1 ms) of one level of `boots` bootstraps under the
+// blind-rotation auto selection (blind_rotate.cu).
+int br_level_cost(int boots);
+// Wave packing of the levelizer (backend.cpp); process-wide, default on
+// (env CVM_PACK=0 turns it off).
+bool level_packing();
+void set_level_packing(bool on);
+
 struct Node {
   GateKind kind;
   bool input;
@@ -181,6 +189,7 @@ class GpuBackend final : public Backend {
   uint64_t take_slot();
   void stage_uploads();
   std::vector<std::vector<cvm_gate>> levels_of(const std::vector<Bit>& ids) const;
+  std::vector<std::vector<cvm_gate>> pack_levels(std::vector<Bit> ids, uint32_t depth) const;
   void run(const std::vector<Bit>& ids);
   void retire(const std::vector<Bit>& done);
 

@@ -103,6 +103,33 @@ def test_wide_level_planner_bit_identical(n, keyset, ctx):
     assert np.array_equal(keyset.decrypt(auto), a & b)
 
 
+@pytest.mark.parametrize("op", ["add", "cmp"])
+def test_wave_packing_same_results(op, keyset, ctx):
+    """The wave-packing levelizer (backend.cpp pack_levels) moves gates
+    between their earliest and latest levels: same number of launches, same
+    ciphertexts as plain dataflow levels, correct decryptions."""
+    from paper_2101_03403_b200._native import lib, check
+    rng = np.random.default_rng(12)
+    batch = 64  # 12,480 (add) / 13,888 (cmp) gates: packing is active
+    av, bv = rng.integers(0, 1 << 16, batch), rng.integers(0, 1 << 16, batch)
+    a = keyset.encrypt_words(av, 16, 91)
+    b = keyset.encrypt_words(bv, 16, 92)
+    old = lib.cvm_get_level_packing()
+    res = {}
+    try:
+        for pack in (1, 0):
+            check(lib.cvm_set_level_packing(pack))
+            res[pack] = P.fu_batch(ctx, op, 16, a, b)
+    finally:
+        check(lib.cvm_set_level_packing(old))
+    (o1, s1), (o0, s0) = res[1], res[0]
+    assert np.array_equal(o1, o0)
+    assert s1["last_flush_levels"] == s0["last_flush_levels"]
+    if op == "add":
+        vals = keyset.decrypt_words(o1.reshape(-1, 631), 17)
+        assert np.array_equal(vals, (av + bv) % (1 << 17))
+
+
 @pytest.mark.parametrize("ks_variant", [1, 6, 7, 8])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
