@@ -279,19 +279,16 @@ std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(const std::vector<Bit>&
   return lv;
 }
 
-// Wave packing.  The number of launches stays the critical path (`depth`
-// dataflow levels), but a gate may run in any launch between its earliest
-// (ASAP) and latest (ALAP) level.  Launch k takes every ready gate whose ALAP
-// level is k, then the most urgent other ready gates (by ALAP level, then
-// id) up to the width the blind-rotation planner runs most efficiently
-// (bootstraps per unit of br_level_cost, plus a fixed per-launch cost for the
-// key switch and launch gaps): e.g. a 256 x ADD16 batch runs as 5 launches of
-// exactly 6 full v4 waves instead of ASAP widths 8192, 8192, 7680, 7424,
-// 6656 (each with a partial wave).  Gates are pure, so the result is
-// unchanged (tests/test_gpu_parity.py compares packed and plain runs).
+// Wave packing (schedule.hpp): the number of launches stays the critical
+// path, but a gate may run in any launch between its earliest (ASAP) and
+// latest (ALAP) level, and launches are filled to the widths the
+// blind-rotation planner runs most efficiently: e.g. a 256 x ADD16 batch runs
+// as five launches of exactly six full v4 waves instead of ASAP widths 8192,
+// 8192, 7680, 7424, 6656 (each with a partial wave).  Gates are pure, so
+// results are unchanged (tests/test_gpu_parity.py compares packed and plain
+// runs; tests/native/schedule_test.cpp checks the schedule's invariants).
 std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(std::vector<Bit> ids,
                                                            uint32_t depth) const {
-  constexpr int kLaunchCost = 3;  // 0.1 ms: key switch + launch gaps per level
   std::sort(ids.begin(), ids.end());  // node ids are a topological order
   const size_t G = ids.size();
   const Bit lo = ids.front(), hi = ids.back();
@@ -306,8 +303,8 @@ std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(std::vector<Bit> ids,
     }
     return (id >= lo && id <= hi) ? local[id - lo] : -1;
   };
-  std::vector<uint32_t> off(G + 1, 0), indeg(G, 0), boots(G), alap(G);
   std::vector<int32_t> pred(3 * G, -1);
+  std::vector<uint8_t> boots(G);
   for (size_t i = 0; i < G; ++i) {
     const Node& n = nodes_[ids[i] - 1];
     boots[i] = n.kind == GateKind::Mux ? 2 : 1;
@@ -315,65 +312,12 @@ std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(std::vector<Bit> ids,
       const int32_t s = src(n.dep[d]);
       bool dup = false;
       for (int e = 0; e < d; ++e) dup |= pred[3 * i + e] == s;
-      if (s >= 0 && !dup) {
-        pred[3 * i + d] = s;
-        ++off[s + 1];
-        ++indeg[i];
-      }
+      if (s >= 0 && !dup) pred[3 * i + d] = s;
     }
   }
-  for (size_t i = 0; i < G; ++i) off[i + 1] += off[i];
-  std::vector<uint32_t> succ(off[G]), fill(off.begin(), off.end() - 1);
-  for (size_t i = 0; i < G; ++i)
-    for (int d = 0; d < 3; ++d)
-      if (pred[3 * i + d] >= 0) succ[fill[pred[3 * i + d]]++] = uint32_t(i);
-  // ALAP level: depth minus the longest gate chain after the gate
-  std::vector<uint32_t> tail(G, 0);
-  for (size_t i = G; i-- > 0;)
-    for (uint32_t e = off[i]; e < off[i + 1]; ++e) tail[i] = std::max(tail[i], tail[succ[e]] + 1);
-  for (size_t i = 0; i < G; ++i) alap[i] = depth - tail[i];
-
+  const std::vector<uint32_t> launch = pack_schedule(pred, boots);
   std::vector<std::vector<cvm_gate>> out(depth);
-  std::vector<uint32_t> ready, next;
-  for (size_t i = 0; i < G; ++i)
-    if (indeg[i] == 0) ready.push_back(uint32_t(i));
-  auto urgent = [&](uint32_t a, uint32_t b) { return alap[a] != alap[b] ? alap[a] < alap[b] : a < b; };
-  for (uint32_t k = 1; k <= depth; ++k) {
-    std::sort(ready.begin(), ready.end(), urgent);
-    int must = 0, avail = 0;
-    for (uint32_t i : ready) {
-      avail += int(boots[i]);
-      if (alap[i] <= k) must += int(boots[i]);
-    }
-    // the most efficient width in [must, avail]: the planner's costs step at
-    // multiples of 74 bootstraps, so only those (and avail) are candidates
-    int width = avail;
-    if (k < depth && avail > must) {
-      double best = -1.0;
-      auto consider = [&](int w) {
-        if (w < std::max(must, 1) || w > avail) return;
-        const double eff = double(w) / double(br_level_cost(w) + kLaunchCost);
-        if (eff > best + 1e-12 || (eff > best - 1e-12 && w > width)) best = eff, width = w;
-      };
-      width = 0;
-      consider(avail);
-      for (int w = 74; w <= avail; w += 74) consider(w);
-      consider(must);
-    }
-    size_t taken = 0;
-    int used = 0;
-    for (; taken < ready.size(); ++taken) {
-      const uint32_t i = ready[taken];
-      if (alap[i] > k && used + int(boots[i]) > width) break;
-      used += int(boots[i]);
-      out[k - 1].push_back(gates_[nodes_[ids[i] - 1].gate_idx]);
-      for (uint32_t e = off[i]; e < off[i + 1]; ++e)
-        if (--indeg[succ[e]] == 0) next.push_back(succ[e]);
-    }
-    ready.erase(ready.begin(), ready.begin() + taken);
-    ready.insert(ready.end(), next.begin(), next.end());
-    next.clear();
-  }
+  for (size_t i = 0; i < G; ++i) out[launch[i] - 1].push_back(gates_[nodes_[ids[i] - 1].gate_idx]);
   out.erase(std::remove_if(out.begin(), out.end(), [](const auto& v) { return v.empty(); }),
             out.end());
   return out;

@@ -938,34 +938,6 @@ bool valid_br_variant(int v) {
          v == 5245 || v == 5246 || v == 5247 || valid_br_v4_variant(v);
 }
 
-// The remainder of a wide level after its full v4 waves: at most one more
-// v4 wave, two v3 rounds and four latency rounds, the cheapest combination
-// that covers it.  Returns its cost in 0.1 ms.
-int br_remainder_plan(int rest, int* n8, int* n4, int* n1) {
-  int best = rest > 0 ? 1 << 30 : 0, b8 = 0, b4 = 0, b1 = 0;
-  for (int a = 0; a <= 1 && rest > 0; ++a)
-    for (int b = 0; b <= 2; ++b)
-      for (int c = 0; c <= 4; ++c) {
-        if (a * kBrWave8 + b * kBrWave4 + c * kBrSms < rest) continue;
-        const int cost = a * kBrT8 + b * kBrT4 + c * kBrT1;
-        if (cost < best) best = cost, b8 = a, b4 = b, b1 = c;
-      }
-  if (n8) *n8 = b8, *n4 = b4, *n1 = b1;
-  return best;
-}
-
-// Device time (0.1 ms) of a level of `boots` bootstraps under the auto
-// selection below -- the cost model the wave-packing levelizer
-// (backend.cpp) fills launches with.
-int br_level_cost(int boots) {
-  if (boots <= 0) return 0;
-  if (boots <= kBrSms / 2) return 16;
-  if (boots <= kBrSms) return kBrT1;
-  if (boots <= 2 * kBrSms) return 48;
-  const int full = boots / kBrWave8;
-  return full * kBrT8 + br_remainder_plan(boots - full * kBrWave8, nullptr, nullptr, nullptr);
-}
-
 cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 const c64* bkf4, const c64* tw4, uint32_t* xout,

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/cvm_gpu.h"
+#include "schedule.hpp"
 #include "tfhe_params.h"
 
 namespace cvm {
@@ -128,9 +129,6 @@ class Region {  // RegionScope (gates.hpp:158-170)
 };
 
 // Node record (the reference DagNode, dag.hpp:33-42, minus cost/region).
-// Device time (0.1 ms) of one level of `boots` bootstraps under the
-// blind-rotation auto selection (blind_rotate.cu).
-int br_level_cost(int boots);
 // Wave packing of the levelizer (backend.cpp); process-wide, default on
 // (env CVM_PACK=0 turns it off).
 bool level_packing();

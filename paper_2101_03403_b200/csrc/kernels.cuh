@@ -6,6 +6,7 @@
 
 #include "fft512.cuh"
 #include "fft512w.cuh"
+#include "schedule.hpp"
 #include "tfhe_params.h"
 
 namespace cvm {
@@ -41,13 +42,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
                                 const c64* bkf4, const c64* tw4, uint32_t* xout,
                                 cudaStream_t s);
 bool valid_br_v4_variant(int v);
-// Auto-selection cost model (measured wave times, 0.1 ms; tools/v4_waves.py):
-// a v4 wave of 8 x 148 bootstraps, a v3 round of 4 x 148, a latency round of
-// 148 (one bootstrap per SM).
-constexpr int kBrSms = 148, kBrWave8 = 8 * kBrSms, kBrWave4 = 4 * kBrSms;
-constexpr int kBrT8 = 113, kBrT4 = 58, kBrT1 = 23;
-int br_remainder_plan(int rest, int* n8, int* n4, int* n1);
-int br_level_cost(int boots);
+// Auto-selection cost model: schedule.hpp.
 cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
                                    const uint32_t* slab, const c64* bkf4, const c64* tw4,
                                    uint32_t* xout, cudaStream_t s);
