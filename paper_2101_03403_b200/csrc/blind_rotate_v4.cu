@@ -220,8 +220,7 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
         // which needs no proxy fence.
         __syncwarp();
         if (l == 0) {
-          __threadfence_block();
-          if (atomicAdd(&sm.cnt[slot], 1u) == unsigned(nw - 1)) {
+          if (atom_add_release_cta(&sm.cnt[slot], 1u) == unsigned(nw - 1)) {
             sm.cnt[slot] = 0;
             if (q + S < kChunks) {
               mbar_expect_tx(&sm.full[slot], kRowBytes);

@@ -54,6 +54,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Shared-memory atomic add with release semantics at CTA scope (orders this
+// thread's earlier shared-memory accesses before the increment, without a
+// full fence); returns the old value.
+__device__ __forceinline__ uint32_t atom_add_release_cta(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(smem_u32(p)), "r"(v)
+               : "memory");
+  return old;
+}
 __device__ __forceinline__ void mbar_init_fence() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
