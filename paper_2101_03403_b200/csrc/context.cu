@@ -114,6 +114,7 @@ class Context {
     cudaFree(ksk_);
     cudaFree(kskb_);
     cudaFree(ksktc_);
+    cudaFree(kspart_);
     cudaFree(slab_);
     cudaFree(xlwe_);
     cudaFree(flush_buf_);
@@ -145,6 +146,7 @@ class Context {
     check(launch_ksk_to_limbs(ksk_, kskb_, stream_), "ksk_to_limbs");
     ++stats_.other_launches;
     if (!ksktc_) check(cudaMalloc(&ksktc_, kKskTcWords * 4), "cudaMalloc(ksktc)");
+    if (!kspart_) check(cudaMalloc(&kspart_, kKsPartWords * 4), "cudaMalloc(kspart)");
     check(launch_ksk_to_tc(ksk_, ksktc_, stream_), "ksk_to_tc");
     ++stats_.other_launches;
     check(cudaStreamSynchronize(stream_), "sync(upload_keys)");
@@ -292,7 +294,7 @@ class Context {
           "blind_rotate_kernel");
     end_prof(p);
     p = begin_prof(1);
-    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, ksktc_, slab_, stream_),
+    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, ksktc_, kspart_, slab_, stream_),
           "key_switch_kernel");
     end_prof(p);
     stats_.br_launches++;
@@ -526,6 +528,7 @@ class Context {
   uint32_t* ksk_ = nullptr;
   uint32_t* kskb_ = nullptr;   // KSK as byte limbs for the mma.sync key switch
   uint32_t* ksktc_ = nullptr;  // the same limbs as tcgen05 B tiles
+  uint32_t* kspart_ = nullptr;  // split-K partials of key-switch variant 9
   uint32_t* slab_ = nullptr;
   uint64_t cap_ = 0;
   uint64_t used_ = 0;

@@ -63,10 +63,10 @@ bool valid_br_variant(int v);
 // Key-switch kernel: 1 = one gate per CTA; 6 = one gate per 948-thread CTA
 // (6 position groups, latency); 7 = the whole level as one INT8 tensor-core
 // product (one-hot digits x byte limbs of the KSK) on mma.sync; 8 = the same
-// product on tcgen05.mma with TMEM accumulators; 0 = auto by level width
-// (6 below kKsTcMinGates gates, else 8).  Env CVM_KS_KERNEL.
+// product on tcgen05.mma with TMEM accumulators; 9 = 8 split along the
+// coefficients (K) into up to 16 CTAs per tile plus a reduction, so a narrow
+// level still fills the GPU; 0 = auto (9).  Env CVM_KS_KERNEL.
 constexpr int kDefaultKsVariant = 0;
-constexpr int kKsTcMinGates = 256;
 int ks_variant();
 void set_ks_variant(int v);
 bool valid_ks_variant(int v);
@@ -81,8 +81,11 @@ constexpr size_t kKskbWords = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
 // (1024 coefficients x 5 column tiles x 4 limbs x 4 KB).
 cudaError_t launch_ksk_to_tc(const uint32_t* ksk, uint32_t* ksktc, cudaStream_t s);
 constexpr size_t kKskTcWords = size_t(kPolyN) * 5 * 4 * 1024;
+// kspart: split-K scratch of variant 9, kKsPartWords u32.
+constexpr int kKsMaxSplits = 16;
+constexpr size_t kKsPartWords = size_t(148 / 5) * 128 * 640;
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, const uint32_t* kskb, const uint32_t* ksktc,
-                              uint32_t* slab, cudaStream_t s);
+                              uint32_t* kspart, uint32_t* slab, cudaStream_t s);
 
 }  // namespace cvm

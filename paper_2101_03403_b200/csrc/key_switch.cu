@@ -382,13 +382,19 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64
       : "memory");
 }
 
+// Split-K (blockIdx.z, `part` non-null): CTA z multiplies coefficients
+// [z*k_per, (z+1)*k_per) only and writes its partial result (mod 2^32) to
+// part[z][gate][col]; ks_reduce_kernel sums the splits.  A narrow level then
+// runs on 16x more CTAs (one 128-gate tile x 5 column tiles is only five).
 __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
     const KsJob* __restrict__ jobs, int count, const uint32_t* __restrict__ xlwe,
-    const uint32_t* __restrict__ ksktc, uint32_t* __restrict__ slab) {
+    const uint32_t* __restrict__ ksktc, uint32_t* __restrict__ slab, int k_per,
+    uint32_t* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   KsTcSmem& sm = *reinterpret_cast<KsTcSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g0 = blockIdx.x * kTcRows, ct = blockIdx.y;
+  const int z = blockIdx.z, k0 = z * k_per, k1 = k0 + k_per;
   const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
 
   if (tid < kTcRows) {
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
     const uint32_t* x0 = xlwe + size_t(jb.x[0]) * kXlweStride;
     const uint32_t* x1 = jb.x[1] != kNoInput ? xlwe + size_t(jb.x[1]) * kXlweStride : nullptr;
     const uint32_t row_off = uint32_t((tid >> 3) * 256 + (tid & 7) * 16);
-    for (int i0 = 0; i0 < kPolyN; i0 += 16) {
+    for (int i0 = k0; i0 < k1; i0 += 16) {
       uint32_t ab[16];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -445,8 +451,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
       }
 #pragma unroll
       for (int ii = 0; ii < 16; ++ii) {
-        const int i = i0 + ii, s = i % kTcStages;
-        if (i >= kTcStages) mbar_wait(&sm.empty[s], ((i / kTcStages) + 1) & 1);
+        const int li = i0 - k0 + ii, s = li % kTcStages;
+        if (li >= kTcStages) mbar_wait(&sm.empty[s], ((li / kTcStages) + 1) & 1);
         uint32_t oh[8];
 #pragma unroll
         for (int j = 0; j < kKsT; ++j) oh[j] = 1u << (8 * ((ab[ii] >> (30 - 2 * j)) & 3u));
@@ -473,22 +479,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
       for (int c = 0; c < 8; ++c) {
         const int col = ct * kTcRows + c0 + c;
         const uint32_t sum = r[0][c] + (r[1][c] << 8) + (r[2][c] << 16) + (r[3][c] << 24);
-        if (g < count && col < kKskRowStride) out[col] = (col == kN ? sm.bval[tid] : 0u) - sum;
+        if (g < count && col < kKskRowStride) {
+          const uint32_t v = (col == kN && z == 0 ? sm.bval[tid] : 0u) - sum;
+          if (part) part[(size_t(z) * gridDim.x * kTcRows + g) * (kTcColTiles * kTcRows) + col] = v;
+          else out[col] = v;
+        }
       }
     }
   } else if (warp == 4) {
     // ---- MMA issuer ----
     if (lane == 0) {
-      for (int i = 0; i < kPolyN; ++i) {
-        const int s = i % kTcStages;
-        const uint32_t par = (i / kTcStages) & 1;
+      for (int li = 0; li < k_per; ++li) {
+        const int s = li % kTcStages;
+        const uint32_t par = (li / kTcStages) & 1;
         mbar_wait(&sm.b_full[s], par);
         mbar_wait(&sm.a_full[s], par);
         tc_fence_after();
         const uint64_t ad = umma_desc_kmajor(sm.a[s]);
 #pragma unroll
         for (int l = 0; l < 4; ++l)
-          umma_i8(tbase + uint32_t(l * kTcRows), ad, umma_desc_kmajor(sm.b[s][l]), i > 0);
+          umma_i8(tbase + uint32_t(l * kTcRows), ad, umma_desc_kmajor(sm.b[s][l]), li > 0);
         tc_commit(&sm.empty[s]);  // frees stage s once these MMAs have read it
       }
       tc_commit(&sm.done);
@@ -497,9 +507,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
   } else {
     // ---- B producer ----
     if (lane == 0) {
-      for (int i = 0; i < kPolyN; ++i) {
-        const int s = i % kTcStages;
-        if (i >= kTcStages) mbar_wait(&sm.empty[s], ((i / kTcStages) + 1) & 1);
+      for (int i = k0; i < k1; ++i) {
+        const int li = i - k0, s = li % kTcStages;
+        if (li >= kTcStages) mbar_wait(&sm.empty[s], ((li / kTcStages) + 1) & 1);
         mbar_expect_tx(&sm.b_full[s], 4 * kTcTileBytes);
         bulk_g2s(sm.b[s], ksktc + (size_t(i) * kTcColTiles + ct) * (4 * kTcTileBytes / 4),
                  4 * kTcTileBytes, &sm.b_full[s]);
@@ -516,6 +526,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) key_switch_tc_kernel(
   }
 }
 
+// Sum of the split-K partials of key_switch_tc_kernel into the output slots.
+__global__ void __launch_bounds__(256) ks_reduce_kernel(const KsJob* __restrict__ jobs,
+                                                        int count, int splits, int rows,
+                                                        const uint32_t* __restrict__ part,
+                                                        uint32_t* __restrict__ slab) {
+  const int g = blockIdx.x;
+  const size_t plane = size_t(rows) * (kTcColTiles * kTcRows);
+  uint32_t* out = slab + size_t(jobs[g].out_slot) * kLweStride;
+  for (int col = threadIdx.x; col < kKskRowStride; col += blockDim.x) {
+    const uint32_t* p = part + size_t(g) * (kTcColTiles * kTcRows) + col;
+    uint32_t v = 0;
+    for (int z = 0; z < splits; ++z) v += p[z * plane];
+    out[col] = v;
+  }
+  (void)count;
+}
+
 // ----------------------------------------------------------- launchers --
 static int g_ks_variant = -1;
 int ks_variant() {
@@ -523,7 +550,7 @@ int ks_variant() {
   return g_ks_variant;
 }
 void set_ks_variant(int v) { g_ks_variant = v; }
-bool valid_ks_variant(int v) { return v == 0 || v == 1 || v == 6 || v == 7 || v == 8; }
+bool valid_ks_variant(int v) { return v == 0 || v == 1 || v == 6 || v == 7 || v == 8 || v == 9; }
 
 cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s) {
   const size_t total = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
@@ -538,14 +565,14 @@ cudaError_t launch_ksk_to_tc(const uint32_t* ksk, uint32_t* ksktc, cudaStream_t 
 
 cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
                               const uint32_t* ksk, const uint32_t* kskb, const uint32_t* ksktc,
-                              uint32_t* slab, cudaStream_t s) {
+                              uint32_t* kspart, uint32_t* slab, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
   int variant = ks_variant();
-  // auto: the 6-group gather kernel on narrow levels (10x faster than one
-  // gate per CTA), the tcgen05 product from 256 gates (equal there, 3.3x the
-  // mma.sync product on wide levels; profiles/r01_variant_sweep.txt)
-  if (variant == 0) variant = count >= kKsTcMinGates ? 8 : 6;
+  // auto: the split-K tcgen05 product at every width (0.037 ms for a
+  // 32-gate level vs 0.178 for the 6-group gather and 0.26 unsplit; equal to
+  // the unsplit product on wide levels; profiles/r01_variant_sweep.txt)
+  if (variant == 0) variant = 9;
   switch (variant) {
     case 1: key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab); break;
     case 6:
@@ -568,7 +595,29 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
       cudaError_t e = set_smem(key_switch_tc_kernel, smem, configured);
       if (e != cudaSuccess) return e;
       const dim3 grid((count + kTcRows - 1) / kTcRows, kTcColTiles);
-      key_switch_tc_kernel<<<grid, kTcThreads, smem, s>>>(jobs, count, xlwe, ksktc, slab);
+      key_switch_tc_kernel<<<grid, kTcThreads, smem, s>>>(jobs, count, xlwe, ksktc, slab,
+                                                           kPolyN, nullptr);
+      break;
+    }
+    case 9: {  // split-K tcgen05 product: ~148 CTAs whatever the level width
+      if (!ksktc || !kspart) return cudaErrorInvalidValue;
+      static bool configured = false;
+      const int smem = int(sizeof(KsTcSmem));
+      cudaError_t e = set_smem(key_switch_tc_kernel, smem, configured);
+      if (e != cudaSuccess) return e;
+      const int mt = (count + kTcRows - 1) / kTcRows;
+      int splits = 1;
+      while (splits < kKsMaxSplits && 2 * splits * mt * kTcColTiles <= 148) splits *= 2;
+      if (splits == 1) {
+        key_switch_tc_kernel<<<dim3(mt, kTcColTiles), kTcThreads, smem, s>>>(
+            jobs, count, xlwe, ksktc, slab, kPolyN, nullptr);
+        break;
+      }
+      key_switch_tc_kernel<<<dim3(mt, kTcColTiles, splits), kTcThreads, smem, s>>>(
+          jobs, count, xlwe, ksktc, slab, kPolyN / splits, kspart);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      ks_reduce_kernel<<<count, 256, 0, s>>>(jobs, count, splits, mt * kTcRows, kspart, slab);
       break;
     }
     default: return cudaErrorInvalidValue;

@@ -130,7 +130,7 @@ def test_wave_packing_same_results(op, keyset, ctx):
         assert np.array_equal(vals, (av + bv) % (1 << 17))
 
 
-@pytest.mark.parametrize("ks_variant", [1, 6, 7, 8])
+@pytest.mark.parametrize("ks_variant", [1, 6, 7, 8, 9])
 def test_key_switch_variants_bit_identical(ks_variant, keyset, ctx, oracle_keys):
     """Single- and multi-gate key-switch kernels, with plain gates and MUX
     (two extracted samples + 1/8) and a partially filled last CTA."""
@@ -258,7 +258,7 @@ def test_key_switch_tensor_core_multi_tile(keyset, ctx):
     outs = {}
     old = lib.cvm_get_ks_variant()
     try:
-        for v in (6, 7, 8):
+        for v in (6, 7, 8, 9):
             check(lib.cvm_set_ks_variant(v))
             ctx.submit_level(gates)
             ctx.sync()
@@ -267,6 +267,7 @@ def test_key_switch_tensor_core_multi_tile(keyset, ctx):
         check(lib.cvm_set_ks_variant(old))
     assert np.array_equal(outs[6], outs[7])
     assert np.array_equal(outs[6], outs[8])
+    assert np.array_equal(outs[6], outs[9])  # split-K over 2 tiles x 5 x 8 CTAs
     bits = keyset.decrypt(outs[7])
     assert np.array_equal(bits[:n], np.where(s == 1, t, f))
     assert np.array_equal(bits[n:], 1 - (s ^ t))
