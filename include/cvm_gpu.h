@@ -170,7 +170,8 @@ CVM_API int cvm_get_level_packing(void);
  * threads (6 position groups, latency); 7 = the level as one INT8
  * tensor-core product (one-hot digits x KSK byte limbs) on mma.sync; 8 = the
  * same product on tcgen05.mma with the limb accumulators in tensor memory;
- * 0 = auto (default: 6 below 256 gates, else 8).  Bit-identical. */
+ * 9 = 8 split along the coefficients over up to 16 CTAs per tile plus a
+ * reduction; 0 = auto (default: 9).  Bit-identical. */
 CVM_API int cvm_set_ks_variant(int variant);
 CVM_API int cvm_get_ks_variant(void);
 
