@@ -151,9 +151,11 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * ring); 5244 / 5245 / 5246 / 5247 = 5144 with each key slot refilled by its
  * last reader (4- to 7-row ring); 9 = one bootstrap on 384 threads (six
  * gadget rows concurrently, latency); 19 = 9 with generated twiddles; 92 = one
- * bootstrap on a 2-SM thread-block cluster; 6000 + 100*(1-hold) + 10*W + S
+ * bootstrap on a 2-SM thread-block cluster; 96 = 92 with the partial
+ * products exchanged by st.async + mbarrier instead of a cluster barrier;
+ * 6000 + 100*(1-hold) + 10*W + S
  * (W = 1..8, S = 4/5; e.g. 6085) = v4, one bootstrap per warp on a warp-wide
- * FFT, W warps per CTA on an S-row key ring.  0 = auto (default): 92 for
+ * FFT, W warps per CTA on an S-row key ring.  0 = auto (default): 96 for
  * levels up to 74 bootstraps, 9 up to 148, 13 up to 296, else full v4 waves
  * (6085) with the remainder on the cheapest mix of one v4 wave, 5247 rounds
  * and 9 rounds.  Every variant computes bit-identical ciphertexts. */

@@ -759,8 +759,17 @@ struct PairSmem {
   uint32_t acc[kPolyN];   // ACC part r
   uint16_t bar[kLweWords + 1];
   uint64_t full[kL];
+  uint64_t rbar[2];  // kAsync: the peer's partial of step parity 0 / 1 landed
 };
 
+// kAsync: the peer's partial product arrives by st.async remote stores that
+// complete a transaction count on this CTA's rbar mbarrier (armed each step
+// with the expected 8 KB), so the consumer waits on a local mbarrier instead
+// of a cluster barrier (whose release fence, MEMBAR.ALL.GPU, and
+// arrive/wait were ~15% of the pair kernel's stall samples).  The receive
+// buffer alternates by step parity; the data dependence through the two
+// accumulator parts keeps the peer from overwriting a buffer still being read.
+template <bool kAsync = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     blind_rotate_pair_kernel(const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
                              const c64* __restrict__ bkf, const c64* __restrict__ tw1,
@@ -778,6 +787,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
 
   if (tid == 0) {
     for (int p = 0; p < kL; ++p) mbar_init(&sm.full[p], 1);
+    mbar_init(&sm.rbar[0], 1);
+    mbar_init(&sm.rbar[1], 1);
     mbar_init_fence();
   }
   __syncthreads();
@@ -801,6 +812,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
       sm.acc[j] = r == 0 ? 0u : ((((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu));
   }
   c64* peer_recv = cluster.map_shared_rank(&sm.recv[0][0][0], r ^ 1);
+  uint32_t peer_recv_a = 0, peer_rbar_a = 0;  // shared::cluster addresses in the peer
+  if constexpr (kAsync) {
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(peer_recv_a)
+                 : "r"(smem_u32(&sm.recv[0][0][0])), "r"(r ^ 1));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(peer_rbar_a)
+                 : "r"(smem_u32(&sm.rbar[0])), "r"(r ^ 1));
+  }
   const int shift = 32 - (g + 1) * kBgBit;
   c64* xb0 = sm.xbuf[g][0];
   c64* xb1 = sm.xbuf[g][1];
@@ -809,6 +829,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
 
   for (int i = 0; i < kN; ++i) {
     __syncthreads();  // ACC part r of the previous step complete
+    if (kAsync && tid == 0) mbar_expect_tx(&sm.rbar[i & 1], 8 * 64 * 16);
     const int ai = sm.bar[i];
     uint32_t dif[16];
     rotated_diff(sm.acc, ai, t, dif);
@@ -836,15 +857,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     if (g == 1) {     // the peer's polynomial: sum over levels, store remotely
       c64* dst = peer_recv + (i & 1) * 512;
 #pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2)
-        dst[k2 * 64 + t] = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
-                                sm.red[2][r ^ 1][k2][t]);
+      for (int k2 = 0; k2 < 8; ++k2) {
+        const c64 x = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
+                           sm.red[2][r ^ 1][k2][t]);
+        if constexpr (kAsync) {
+          const uint32_t a = peer_recv_a + uint32_t(((i & 1) * 512 + k2 * 64 + t) * 16);
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, "
+              "[%3];" ::"r"(a),
+              "l"(__double_as_longlong(x.x)), "l"(__double_as_longlong(x.y)),
+              "r"(peer_rbar_a + uint32_t(8 * (i & 1)))
+              : "memory");
+        } else {
+          dst[k2 * 64 + t] = x;
+        }
+      }
     } else if (g == 0) {  // my polynomial: local part of the sum
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2)
         v[k2] = cadd(cadd(sm.red[0][r][k2][t], sm.red[1][r][k2][t]), sm.red[2][r][k2][t]);
     }
-    cluster.sync();  // partial products exchanged
+    if constexpr (kAsync) {
+      if (g == 0) mbar_wait(&sm.rbar[i & 1], (i >> 1) & 1);  // the peer's partial landed
+    } else {
+      cluster.sync();  // partial products exchanged
+    }
     if (g == 0) {
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) v[k2] = cadd(v[k2], sm.recv[i & 1][k2][t]);
@@ -912,14 +949,16 @@ static cudaError_t launch_wide(const BrJob* jobs, int count, const uint32_t* sla
   return cudaGetLastError();
 }
 
+template <bool kAsync = false>
 static cudaError_t launch_pair(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
   static bool configured = false;
   const int smem = int(sizeof(PairSmem));
-  cudaError_t e = set_smem(blind_rotate_pair_kernel, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_pair_kernel<kAsync>, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_pair_kernel<<<2 * count, 64 * kL, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
+  blind_rotate_pair_kernel<kAsync><<<2 * count, 64 * kL, smem, s>>>(jobs, slab, bkf, tw1, tw2,
+                                                                   xout);
   return cudaGetLastError();
 }
 
@@ -931,7 +970,8 @@ int br_variant() {
 void set_br_variant(int v) { g_br_variant = v; }
 int default_br_variant() { return kDefaultBrVariant; }
 bool valid_br_variant(int v) {
-  return v == 0 || v == 1 || v == 9 || v == 19 || v == 92 || v == 13 || v == 22 || v == 23 ||
+  return v == 0 || v == 1 || v == 9 || v == 19 || v == 92 || v == 96 || v == 13 || v == 22 ||
+         v == 23 ||
          v == 43 ||
          v == 3044 || v == 4044 ||
          v == 5044 || v == 5054 || v == 5063 || v == 5144 || v == 5146 || v == 5244 ||
@@ -953,7 +993,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     // kernel (blind_rotate_v4.cu) with the remainder split off below.
     constexpr int kSms = kBrSms;
     if (count <= kSms / 2) {
-      variant = 92;  // one bootstrap per 2-SM cluster: 1.62 vs 2.27 ms
+      variant = 96;  // one bootstrap per 2-SM cluster: 1.53 vs 2.27 ms
     } else if (count <= kSms) {
       variant = 9;
     } else if (count <= 2 * kSms) {
@@ -1002,6 +1042,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     case 9: return launch_wide(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 19: return launch_wide<true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 92: return launch_pair(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 96: return launch_pair<true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 13: return launch_v2<1, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 22: return launch_v2<2, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
     case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);

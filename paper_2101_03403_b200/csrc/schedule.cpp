@@ -20,7 +20,7 @@ int br_remainder_plan(int rest, int* n8, int* n4, int* n1) {
 
 int br_level_cost(int boots) {
   if (boots <= 0) return 0;
-  if (boots <= kBrSms / 2) return 16;  // pair kernel, 1.6 ms
+  if (boots <= kBrSms / 2) return 15;  // pair kernel, 1.53 ms
   if (boots <= kBrSms) return kBrT1;   // one bootstrap per SM
   if (boots <= 2 * kBrSms) return 48;  // one bootstrap per 64-thread CTA
   const int full = boots / kBrWave8;

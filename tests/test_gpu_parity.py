@@ -45,7 +45,7 @@ def test_nand_level_bit_exact(keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), 1 - (a & b))
 
 
-@pytest.mark.parametrize("variant", [1, 9, 19, 92, 13, 22, 23, 43, 3044, 4044, 5044, 5054, 5063,
+@pytest.mark.parametrize("variant", [1, 9, 19, 92, 96, 13, 22, 23, 43, 3044, 4044, 5044, 5054, 5063,
                                      5144, 5146, 5244, 5246, 5247, 6185, 6085, 6035])
 def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     """Every blind-rotation kernel variant (one gate per CTA via L1, G gates per
