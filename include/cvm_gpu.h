@@ -156,7 +156,7 @@ CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
  * 6000 + 100*(1-hold) + 10*W + S
  * (W = 1..8, S = 4/5; e.g. 6085) = v4, one bootstrap per warp on a warp-wide
  * FFT, W warps per CTA on an S-row key ring.  0 = auto (default): 96 for
- * levels up to 74 bootstraps, 9 up to 148, 13 up to 296, else full v4 waves
+ * levels up to 74 bootstraps, 9 up to 296, else full v4 waves
  * (6085) with the remainder on the cheapest mix of one v4 wave, 5247 rounds
  * and 9 rounds.  Every variant computes bit-identical ciphertexts. */
 CVM_API int cvm_set_br_variant(int variant);

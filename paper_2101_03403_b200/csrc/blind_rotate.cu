@@ -994,10 +994,8 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     constexpr int kSms = kBrSms;
     if (count <= kSms / 2) {
       variant = 96;  // one bootstrap per 2-SM cluster: 1.53 vs 2.27 ms
-    } else if (count <= kSms) {
-      variant = 9;
     } else if (count <= 2 * kSms) {
-      variant = 13;
+      variant = 9;  // one or two rounds of one bootstrap per SM (4.55 ms for 296; v2: 4.82)
     } else {
       // Wide levels: the v4 kernel (one bootstrap per warp, 8 per SM) works
       // in waves of 8 x 148 bootstraps (~11.4 ms; with 5-7 warps per SM a

@@ -21,8 +21,8 @@ int br_remainder_plan(int rest, int* n8, int* n4, int* n1) {
 int br_level_cost(int boots) {
   if (boots <= 0) return 0;
   if (boots <= kBrSms / 2) return 15;  // pair kernel, 1.53 ms
-  if (boots <= kBrSms) return kBrT1;   // one bootstrap per SM
-  if (boots <= 2 * kBrSms) return 48;  // one bootstrap per 64-thread CTA
+  if (boots <= kBrSms) return kBrT1;       // one bootstrap per SM
+  if (boots <= 2 * kBrSms) return 2 * kBrT1;  // two rounds of it
   const int full = boots / kBrWave8;
   return full * kBrT8 + br_remainder_plan(boots - full * kBrWave8, nullptr, nullptr, nullptr);
 }
