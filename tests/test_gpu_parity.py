@@ -103,6 +103,37 @@ def test_wide_level_planner_bit_identical(n, keyset, ctx):
     assert np.array_equal(keyset.decrypt(auto), a & b)
 
 
+def test_wide_mux_level_auto_vs_pinned(keyset, ctx):
+    """A wide MUX level (700 gates = 1,400 blind rotations: a full v4 wave plus
+    a remainder, then the split-K key switch over 6 tiles with two extracted
+    samples per gate) under the auto selection equals the same level on
+    pinned kernels (v4 6085 + unsplit tcgen05 key switch), and decrypts."""
+    from paper_2101_03403_b200._native import lib, check
+    n = 700
+    s, t, f = _bits(n, 50), _bits(n, 51), _bits(n, 52)
+    cs, ct, cf = keyset.encrypt(s, 93), keyset.encrypt(t, 94), keyset.encrypt(f, 95)
+    base = ctx.alloc(5 * n)
+    for k, c in enumerate((cs, ct, cf)):
+        ctx.upload(base + k * n, c)
+    mux = lambda dst: [("MUX", [(base + i, 1, 0), (base + n + i, 1, 0),  # noqa: E731
+                                (base + 2 * n + i, 1, 0)], dst + i) for i in range(n)]
+    ob, ok = lib.cvm_get_br_variant(), lib.cvm_get_ks_variant()
+    try:
+        check(lib.cvm_set_br_variant(0))
+        check(lib.cvm_set_ks_variant(0))
+        ctx.submit_level(mux(base + 3 * n))
+        check(lib.cvm_set_br_variant(6085))
+        check(lib.cvm_set_ks_variant(8))
+        ctx.submit_level(mux(base + 4 * n))
+        ctx.sync()
+    finally:
+        check(lib.cvm_set_br_variant(ob))
+        check(lib.cvm_set_ks_variant(ok))
+    auto, pinned = ctx.download(base + 3 * n, n), ctx.download(base + 4 * n, n)
+    assert np.array_equal(auto, pinned)
+    assert np.array_equal(keyset.decrypt(auto), np.where(s == 1, t, f))
+
+
 @pytest.mark.parametrize("op", ["add", "cmp"])
 def test_wave_packing_same_results(op, keyset, ctx):
     """The wave-packing levelizer (backend.cpp pack_levels) moves gates
