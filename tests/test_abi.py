@@ -47,6 +47,36 @@ def test_version_and_errors():
     assert b"null" in N.lib.cvm_last_error()
 
 
+def test_process_wide_kernel_knobs():
+    """Variant / packing setters validate their argument (host-only, no GPU):
+    every documented value is accepted and restored, anything else raises
+    InputError and leaves the setting unchanged."""
+    lib = N.lib
+    br, ks, pack = lib.cvm_get_br_variant(), lib.cvm_get_ks_variant(), lib.cvm_get_level_packing()
+    try:
+        for v in (0, 1, 9, 13, 92, 96, 5247, 6085, 6185, 6015, 6084):
+            N.check(lib.cvm_set_br_variant(v))
+            assert lib.cvm_get_br_variant() == v
+        for v in (2, 7000, 6095, 6086, 6485):
+            with pytest.raises(P.CvmInputError):
+                N.check(lib.cvm_set_br_variant(v))
+            assert lib.cvm_get_br_variant() == 6084
+        for v in (0, 1, 6, 7, 8, 9):
+            N.check(lib.cvm_set_ks_variant(v))
+            assert lib.cvm_get_ks_variant() == v
+        with pytest.raises(P.CvmInputError):
+            N.check(lib.cvm_set_ks_variant(5))
+        for v in (0, 1):
+            N.check(lib.cvm_set_level_packing(v))
+            assert lib.cvm_get_level_packing() == v
+        with pytest.raises(P.CvmInputError):
+            N.check(lib.cvm_set_level_packing(2))
+    finally:
+        N.check(lib.cvm_set_br_variant(br))
+        N.check(lib.cvm_set_ks_variant(ks))
+        N.check(lib.cvm_set_level_packing(pack))
+
+
 def _has_gpu():
     try:
         import torch
