@@ -6,28 +6,34 @@ on): 256 independent 16-bit homomorphic ADDs (Kogge-Stone, 195 bootstrapped
 gates each, 9 dataflow levels -> 49,920 bootstraps per step), n=630, N=1024,
 l=3, Bg=2^7, t=8, base 4, torus32, seeded synthetic operands (no dataset is
 involved; inputs are uniform random 16-bit integers encrypted under seeded keys).
+The adder circuit is the reference's own alu::add, recorded once by the
+reference code (integration/refshim.py -> libcvm_refshim.so) and replayed by
+the B200 library (cvm_backend_replay_dag / cvm_dag_batch).
 
   value   bootstrapped gates/s with inputs resident in HBM: one step = the
-          recorded 9-level plan replayed on the device (18 launches).
-  e2e     the same metric through the public C-ABI call cvm_fu_batch with host
-          buffers: pinned H2D of the 512 operand words (20.7 MB), circuit
-          recording, levelised execution, D2H of the 256 x 17 result bits.
-          cvm_fu_batch evaluates only the outputs' cone (180 of 195 gates per
-          ADD16), so e2e counts the gates it executes; ADD16/s is reported
-          beside it.
-  roofline  blind_rotate_kernel (dominant): algorithmic FP64 flops per
-          bootstrap (147,087,360) x bootstraps /
-          summed kernel event time, against the FP64 DFMA peak measured live.
+          recorded 256-adder plan replayed on the device.
+  e2e     the same metric through the public C-ABI call cvm_dag_batch with host
+          buffers: pinned H2D of the 512 operand words (20.7 MB), replay of the
+          recorded table, levelised execution, D2H of the 256 x 17 result bits.
+          cvm_dag_batch evaluates only the outputs' cone (180 of 195 gates per
+          ADD16), so e2e counts the gates it executes; ADD16/s is beside it.
+          e2e.reference_api: the reference's own API through the drop-in
+          (Word::encrypt, alu::add on cryptovm::GpuBackend, decrypt_word per
+          result; host encryption and decryption inside the timed region).
+  roofline  the blind-rotation kernels (99% of the device time): algorithmic
+          FP64 flops per bootstrap (147,087,360) x
+          bootstraps / summed kernel event time, against the FP64 DFMA peak
+          measured live (MEASURED_PEAKS.json has no FP64 figure).
 
 Multi-GPU (--gpus N under torchrun): weak scaling, each rank runs its own 256
 independent adders (no data-path collective; gates of a level are
 independent), barrier + max-over-ranks device time.
 
 --impl reference: the reference's path on the host CPU.  The reference ships
-no TFHE code, so this arm times the CPU restatement of
-the TFHE library's gate bootstrapping (oracle/, double-precision FFT: the
-library's own method) on all host threads, on a bounded sample of the same
-workload (the first dataflow level's AND/XOR gates).
+no TFHE code, so this arm times the CPU restatement
+of the TFHE library's gate bootstrapping (oracle/, double-precision FFT: the
+library's own method) on all host threads, evaluating whole ADD16 circuits
+(the same recorded DAG, several adders level by level in lockstep).
 """
 import argparse
 import json
@@ -48,6 +54,7 @@ WIDTH, BATCH = 16, 256
 GATES_PER_ADD = 195
 METRIC = "bootstrapped gates/s (batched) on 1 B200; 16-bit FHE ADD ops/s & latency"
 KEY_SEED, DATA_SEED = 20260808, 4242
+USES_C = {"add_cin", "addsub"}
 
 
 def dist_env():
@@ -112,133 +119,201 @@ def workload_operands(rank):
     return rng.integers(0, 1 << WIDTH, BATCH), rng.integers(0, 1 << WIDTH, BATCH)
 
 
+# --------------------------------------------------------- recorded circuits --
+def load_dag(op, width):
+    """The unit's gate table as the reference records it: live from the
+    reference code (integration/_build/libcvm_refshim.so); if that library
+    was not built, the same table the reference run stored in
+    tests/golden/dags.npz (tests/golden/make_golden.py)."""
+    import paper_2101_03403_b200 as P
+    sys.path.insert(0, os.path.join(REPO, "integration"))
+    import refshim
+    if refshim.available():
+        d = refshim.record_fu(op, width)
+        d.source = "reference alu recorded live (libcvm_refshim.so)"
+        return d
+    g = np.load(os.path.join(REPO, "tests", "golden", "dags.npz"))
+    src = "umul" if op == "mul_lo" else op
+    outs = g[f"{src}_{width}_out"][:width] if op == "mul_lo" else g[f"{src}_{width}_out"]
+    d = P.Dag.from_rows(g[f"{src}_{width}_nodes"], outs, f"{op}{width}")
+    d.source = "reference alu table from tests/golden/dags.npz"
+    return d
+
+
+def operand_lwe(ks, op, width, av, bv, seed, cv=None):
+    """(batch, n_inputs, 631): a's bits, b's bits (LSB first)[, c]."""
+    parts = [ks.encrypt_words(av, width, seed), ks.encrypt_words(bv, width, seed + 1)]
+    if op in USES_C:
+        parts.append(ks.encrypt(np.asarray(cv, np.uint8), seed + 2).reshape(-1, 1, 631))
+    return np.concatenate(parts, axis=1)
+
+
+def replicate_rows(rows, k):
+    """k independent copies of a gate table ((n, 7) oracle layout) in one."""
+    n = len(rows)
+    out = np.tile(rows, (k, 1))
+    for i in range(1, k):
+        blk = out[i * n:(i + 1) * n]
+        dep = blk[:, 3:6]
+        blk[:, 3:6] = np.where(dep > 0, dep + i * n, 0)
+    return out
+
+
 # ------------------------------------------------------------ CPU baseline --
-def cpu_sample_inputs(sk, n_gates, seed=7):
-    """First dataflow level of the ADD16 batch: per bit an AND and an XOR of
-    the two operand bits (alu.cpp:106-108), as fresh ciphertexts under the
-    oracle's keys (same seed, same key bytes as the product keygen)."""
-    import oracle as O
-    rng = np.random.default_rng(seed)
-    bits_a = rng.integers(0, 2, n_gates).astype(np.uint8)
-    bits_b = rng.integers(0, 2, n_gates).astype(np.uint8)
-    a, b = sk.encrypt(bits_a, 1), sk.encrypt(bits_b, 2)
-    kinds = np.where(np.arange(n_gates) % 2 == 0, O.AND, O.XOR).astype(np.uint8)
-    return kinds, a, b
-
-
-def cpu_model():
+def cpu_info():
+    info = {"cpu_model": "unknown", "nproc": os.cpu_count()}
     try:
         with open("/proc/cpuinfo") as f:
             for line in f:
                 if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
     except OSError:
         pass
-    return "unknown"
+    try:
+        import psutil
+        info["physical_cores"] = psutil.cpu_count(logical=False)
+        info["logical_cpus"] = psutil.cpu_count(logical=True)
+    except Exception:
+        pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=5).stdout
+        for line in out.splitlines():
+            if line.startswith("Thread(s) per core"):
+                info["threads_per_core"] = int(line.split(":")[1])
+    except Exception:
+        pass
+    return info
 
 
-def cpu_baseline(target_s=12.0, threads=None):
-    """Oracle (double-FFT TFHE, the library's method) on all host threads."""
+def cpu_add16_circuits(adders, threads, rounds=1):
+    """The oracle (double-FFT TFHE, the library's method) evaluating `adders`
+    whole ADD16 circuits (the reference's recorded DAG) level by level, all
+    adders of a level in one multi-threaded lockstep batch.  Returns
+    (bootstrapped gates per second, seconds, gates evaluated, decrypted ok)."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as O
-    threads = threads or os.cpu_count() or 1
     sk = O.SecretKeys(KEY_SEED)
     ck = O.CloudKeys(sk.bk, sk.ksk, O.MODE_FFT)
-    kinds, a, b = cpu_sample_inputs(sk, threads)
+    dag = load_dag("add", WIDTH)
+    rows = replicate_rows(dag.rows(), adders)
+    rng = np.random.default_rng(7)
+    av, bv = rng.integers(0, 1 << WIDTH, adders), rng.integers(0, 1 << WIDTH, adders)
+    lanes = np.arange(WIDTH)
+    bits = np.concatenate([np.concatenate([(av[i] >> lanes) & 1, (bv[i] >> lanes) & 1])
+                           for i in range(adders)]).astype(np.uint8)
+    cts = sk.encrypt(bits, 8)
     t = time.perf_counter()
-    ck.gates(kinds, a, b, threads=threads)  # calibration, one gate per thread
-    per_round = time.perf_counter() - t
-    rounds = max(1, int(target_s / max(per_round, 1e-3)))
-    n = threads * rounds
-    kinds, a, b = cpu_sample_inputs(sk, n)
-    t = time.perf_counter()
-    out = ck.gates(kinds, a, b, threads=threads)
+    for _ in range(rounds):
+        ct = O.eval_dag(ck, rows, cts, threads)
     dt = time.perf_counter() - t
-    dec = sk.decrypt(out)
-    return {"value": n / dt, "unit": "bootstrapped gates/s", "cores": threads,
-            "kind": "port", "seconds": dt, "cpu_model": cpu_model(),
-            "nproc": os.cpu_count(),
-            "sample": f"{n} AND/XOR gates of the ADD16 batch's first dataflow level, "
-                      f"oracle/ double-FFT TFHE (the TFHE library's method), {threads} threads",
-            "decrypt_sanity": int(dec.size)}
+    outs = np.concatenate([dag.outputs.astype(np.int64) - 1 + i * dag.n_nodes
+                           for i in range(adders)])
+    dec = sk.decrypt(ct[outs]).reshape(adders, WIDTH + 1).astype(np.int64)
+    ok = bool(np.array_equal((dec << np.arange(WIDTH + 1)).sum(axis=1), av + bv))
+    gates = adders * dag.bootstrapped() * rounds
+    return gates / dt, dt, gates, ok
+
+
+def cpu_baseline():
+    """Bounded CPU sample on rank 0 at N=1: whole ADD16 circuits on the
+    oracle with every host thread (about 10-20 s)."""
+    info = cpu_info()
+    threads = os.cpu_count() or 1
+    adders = int(os.environ.get("CPU_ADDERS", max(4, threads)))
+    rate, dt, gates, ok = cpu_add16_circuits(adders, threads)
+    return {"value": rate, "unit": "bootstrapped gates/s", "cores": threads, "kind": "port",
+            "seconds": dt, **info,
+            "sample": f"{adders} whole ADD16 circuits ({gates} bootstrapped gates, all 9 "
+                      f"levels, adders in lockstep per level), oracle/ double-FFT TFHE "
+                      f"(the TFHE library's method), {threads} threads",
+            "add16_ops_per_s": rate / GATES_PER_ADD, "decrypted_correct": ok}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle as O
     threads = os.cpu_count() or 1
-    sk = O.SecretKeys(KEY_SEED)
-    ck = O.CloudKeys(sk.bk, sk.ksk, O.MODE_FFT)
-    # 32 gates per thread per step, evaluated in lockstep (the oracle's batched
-    # mode): enough bootstraps that thread start-up and the per-CMux-step
-    # barrier do not depress the CPU rate, short enough for a few-minute run
-    n = threads * int(os.environ.get("REF_ROUNDS", "32"))
-    kinds, a, b = cpu_sample_inputs(sk, n)
+    adders = int(os.environ.get("REF_ADDERS", max(4, threads)))
+    cpu_add16_circuits(max(1, adders // 4), threads)  # warm-up: keys, caches
+    times, gates, ok = [], 0, True
     for _ in range(args.warmup):
-        ck.gates(kinds[:threads], a[:threads], b[:threads], threads=threads)
-    times = []
+        cpu_add16_circuits(1, threads)
     for _ in range(args.steps):
-        t = time.perf_counter()
-        ck.gates(kinds, a, b, threads=threads)
-        times.append(time.perf_counter() - t)
+        rate, dt, g, good = cpu_add16_circuits(adders, threads)
+        times.append(dt)
+        gates += g
+        ok &= good
     total = sum(times)
-    value = n * args.steps / total
+    value = gates / total
+    info = cpu_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "bootstrapped gates/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32 torus / f64 FFT", "data": "synthetic",
-        "config": {"workload": "config2: 256 x ADD16 (n=630,N=1024,l=3,Bg=2^7,t=8,base 4)",
-                   "sample_per_step": f"{n} gates of the first dataflow level",
+        "config": {"workload": "config2: ADD16 circuits (n=630,N=1024,l=3,Bg=2^7,t=8,base 4)",
+                   "sample_per_step": f"{adders} whole ADD16 circuits "
+                                      f"({adders * GATES_PER_ADD} bootstraps, 9 levels)",
                    "parallelism": f"cpu threads={threads}"},
+        "add16_ops_per_s": value / GATES_PER_ADD,
         "cpu_baseline": {"value": value, "unit": "bootstrapped gates/s", "cores": threads,
-                         "kind": "port", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
-                         "sample": f"{n} AND/XOR gates per step, double-FFT TFHE (oracle/)"},
+                         "kind": "port", **info, "decrypted_correct": ok,
+                         "sample": f"{adders} ADD16 circuits per step, double-FFT TFHE "
+                                   f"(oracle/), adders in lockstep per level"},
         "e2e": {"value": value, "unit": "bootstrapped gates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "note": "reference repo has no TFHE implementation (cleartext SimBackend only); "
-                "this arm is the CPU restatement of the TFHE library's bootstrapping",
+                "this arm is the CPU restatement of the TFHE library's bootstrapping "
+                "evaluating the reference's recorded ADD16 circuit",
     }
     print(json.dumps(line))
     return 0
 
 
 # ------------------------------------------------------- other configs ---
-def extra_configs(P, ctx, ks):
-    """Configs 1, 3, 4 and 5 (BASELINE.json configs[0,2,3,4]) run once each
-    through the public batched API (host buffers in and out), with the device
-    time of their kernels; reported beside the headline config-2 line."""
-    import json as _json
+# (op, batch, reference for the decrypted check)
+EXTRA_OPS = [
+    ("sub", 256, lambda a, b, w: (a - b) % (1 << w), WIDTH),
+    ("cmp", 256, lambda a, b, w: (a - b) % (1 << w), WIDTH),
+    ("and", 256, lambda a, b, w: a & b, WIDTH),
+    ("orr", 256, lambda a, b, w: a | b, WIDTH),
+    ("eor", 256, lambda a, b, w: a ^ b, WIDTH),
+    ("lsl", 256, lambda a, b, w: (a << (b % w)) % (1 << w), WIDTH),
+    ("lsr", 256, lambda a, b, w: a >> (b % w), WIDTH),
+    ("mul_lo", 64, lambda a, b, w: (a * b) % (1 << w), WIDTH),
+    ("umul", 64, lambda a, b, w: a * b, 2 * WIDTH),
+    ("udiv", 16, lambda a, b, w: a // b, WIDTH),
+]
+
+
+def extra_configs(P, ctx, ks, fp64_peak):
+    """Configs 1, 3, 4 and 5 (BASELINE.json configs[0,2,3,4]) plus the other
+    16-bit units, each run once through the public batched API (host buffers
+    in and out, cvm_dag_batch) with the device time of its kernels, its
+    batch-1 latency, its roofline fraction, and the reference's cleartext
+    SimBackend on the same circuit; reported beside the headline line."""
+    sys.path.insert(0, os.path.join(REPO, "integration"))
+    import refshim
     rng = np.random.default_rng(77)
     out = {}
-    # cvm_fu_batch returns its scratch slots, so the slab only holds the
-    # largest single call; size it once for config 4 (216k gates + inputs)
-    # instead of growing it by doubling inside a timed call.
+    # cvm_dag_batch returns its scratch slots, so the slab only holds the
+    # largest single call; size it once (config 4: 216k gates + inputs).
     ctx.reserve(ctx.alloc(0) + 300_000)
+    ctx.set_profiling(True)
 
-    def fu(op, batch, seed):
-        av = rng.integers(0, 1 << WIDTH, batch)
-        bv = rng.integers(0, 1 << WIDTH, batch)
-        a = ks.encrypt_words(av, WIDTH, seed)
-        b = ks.encrypt_words(bv, WIDTH, seed + 1)
+    def frac(boots, ms):
+        return boots * ALG_FLOP_PER_BOOTSTRAP / (ms * 1e-3) / 1e12 / fp64_peak
+
+    def run(dag, lwe):
         ctx.reset_stats()
         t = time.perf_counter()
-        res, st = P.fu_batch(ctx, op, WIDTH, a, b)
+        res, st = P.dag_batch(ctx, dag, lwe)
         wall = time.perf_counter() - t
         k = ctx.kernel_stats()
-        dev_ms = k["br_ms"] + k["ks_ms"]
-        return av, bv, res, {"batch": batch, "recorded_gates": st["bootstrapped"],
-                             "executed_gates": st["executed"],
-                             "levels": st["last_flush_levels"], "wall_s": wall,
-                             "device_ms": dev_ms,
-                             "ops_per_s_e2e": batch / wall,
-                             "ops_per_s_device": batch / (dev_ms * 1e-3),
-                             "gates_per_s_device": st["executed"] / (dev_ms * 1e-3)}
+        return res, st, wall, k["br_ms"] + k["ks_ms"], k["br_ms"]
 
-    ctx.set_profiling(True)
     # config 1: 4096 independent NAND, one level
     n = 4096
     a_bits, b_bits = rng.integers(0, 2, n), rng.integers(0, 2, n)
@@ -251,63 +326,80 @@ def extra_configs(P, ctx, ks):
     ctx.sync()
     k = ctx.kernel_stats()
     ok = np.array_equal(ks.decrypt(ctx.download(base + 2 * n, n)), 1 - (a_bits & b_bits))
-    out["config1_nand4096"] = {"gates_per_s_device": n / ((k["br_ms"] + k["ks_ms"]) * 1e-3),
-                               "device_ms": k["br_ms"] + k["ks_ms"], "correct": bool(ok)}
-    # config 3: SUBS/CMP (sub + NZCV) and LSL by an encrypted amount, 256 each
-    def latency1(op, seed):
-        """Device time of one unit alone (batch 1: the latency kernels)."""
-        return fu(op, 1, seed)[3]["device_ms"]
-
-    av, bv, res, d = fu("cmp", 256, 910)
-    vals = ks.decrypt_words(res[:, :WIDTH].reshape(-1, 631), WIDTH)
-    d["correct"] = bool(np.array_equal(vals, (av - bv) % (1 << WIDTH)))
-    d["latency_batch1_ms"] = latency1("cmp", 915)
-    out["config3_cmp16"] = d
-    av, bv, res, d = fu("lsl", 256, 920)
-    vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
-    d["correct"] = bool(np.array_equal(vals, (av << (bv % WIDTH)) % (1 << WIDTH)))
-    d["bootstraps_per_s_device"] = 2 * d["gates_per_s_device"]  # MUX = 2 bootstraps
-    d["latency_batch1_ms"] = latency1("lsl", 925)
-    out["config3_lsl16"] = d
-    # config 4: 64 x MUL16 producing the low 16 bits (the emulator's MUL):
-    # the high half's 2,083 gates per multiplier are dead and never run
-    av, bv, res, d = fu("mul_lo", 64, 930)
-    vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH)
-    d["correct"] = bool(np.array_equal(vals, (av * bv) % (1 << WIDTH)))
-    d["latency_batch1_ms"] = latency1("mul_lo", 935)
-    out["config4_mul16"] = d
-    av, bv, res, d = fu("umul", 64, 931)
-    vals = ks.decrypt_words(res.reshape(-1, 631), 2 * WIDTH)
-    d["correct"] = bool(np.array_equal(vals, av * bv))
-    out["config4_mul16_full_product"] = d
-    # config 5: a seeded 64-instruction program + UDIV on 8 encrypted registers
-    meta = _json.load(open(os.path.join(REPO, "tests", "golden", "programs.json")))[0]
-    bk = P.Backend(ctx, ks)
-    mem = [bk.import_lwe(w) for w in ks.encrypt_words(meta["mem"], WIDTH, 940)]
-    regs, nzcv = bk.machine_run([tuple(i) for i in meta["insns"]], mem)
-    ctx.reset_stats()
-    t = time.perf_counter()
-    # the key owner reads the final register file and flags: one flush that
-    # evaluates the live cone only
-    bits = bk.decrypt_bits(np.concatenate([regs.ravel(), nzcv]))
-    wall = time.perf_counter() - t
-    k = ctx.kernel_stats()
-    st = bk.stats()
-    words = bits[:8 * WIDTH].reshape(8, WIDTH).astype(np.int64)
-    vals = [int((w << np.arange(WIDTH)).sum()) for w in words]
-    ok = vals == meta["regs"] and list(bits[8 * WIDTH:]) == meta["nzcv"]
-    out["config5_program"] = {"instructions": len(meta["insns"]),
-                              "recorded_gates": st["bootstrapped"],
-                              "executed_gates": st["executed"],
-                              "dataflow_levels": st["last_flush_levels"],
-                              "latency_s": wall, "device_ms": k["br_ms"] + k["ks_ms"],
-                              "instructions_per_s": len(meta["insns"]) / wall,
-                              "correct": bool(ok)}
+    dev = k["br_ms"] + k["ks_ms"]
+    out["config1_nand4096"] = {"gates_per_s_device": n / (dev * 1e-3), "device_ms": dev,
+                               "roofline_frac": frac(n, k["br_ms"]), "correct": bool(ok)}
+    for op, batch, want, ow in EXTRA_OPS:
+        dag = load_dag(op, WIDTH)
+        av = rng.integers(0, 1 << WIDTH, batch)
+        bv = rng.integers(1 if op == "udiv" else 0, 1 << WIDTH, batch)
+        lwe = operand_lwe(ks, op, WIDTH, av, bv, 910 + 10 * len(out))
+        run(dag, lwe[:2])  # first use of this table's kernel shapes: untimed
+        res, st, wall, dev, br = run(dag, lwe)
+        # the value bits (SUB / CMP also return carry or NZCV after them)
+        vals = ks.decrypt_words(np.ascontiguousarray(res[:, :ow]).reshape(-1, 631), ow)
+        boots = st["executed_bootstraps"]
+        d = {"batch": batch, "recorded_gates": st["bootstrapped"],
+             "executed_gates": st["executed"], "executed_bootstraps": boots,
+             "levels": st["last_flush_levels"], "wall_s": wall, "device_ms": dev,
+             "ops_per_s_e2e": batch / wall, "ops_per_s_device": batch / (dev * 1e-3),
+             "gates_per_s_device": st["executed"] / (dev * 1e-3),
+             "bootstraps_per_s_device": boots / (dev * 1e-3),
+             "roofline_frac": frac(boots, br),
+             "correct": bool(np.array_equal(vals, want(av, bv, WIDTH)))}
+        # batch-1 latency: one unit alone (the latency kernels)
+        _, _, w1, dev1, _ = run(dag, lwe[:1])
+        d["latency_batch1_ms_device"], d["latency_batch1_ms_wall"] = dev1, 1e3 * w1
+        # the reference's own CPU path on the same circuit (cleartext booleans)
+        sim_out, sim_s, nodes = refshim.sim_fu_batch(op, WIDTH, av, bv) \
+            if refshim.available() else (None, None, None)
+        if sim_s:
+            d["reference_simbackend"] = {"gates_per_s": st["bootstrapped"] / sim_s,
+                                         "ops_per_s": batch / sim_s, "dag_nodes": nodes,
+                                         "note": "cleartext booleans, not FHE work"}
+        out[f"{op}16"] = d
+    # config 5: the golden seeded 64-instruction program + UDIV on 8 encrypted
+    # registers, recorded by the reference Machine (dataflow across fences)
+    meta = json.load(open(os.path.join(REPO, "tests", "golden", "programs.json")))[0]
+    prog = [tuple(i) for i in meta["insns"]]
+    if refshim.available():
+        dag = refshim.record_program(prog, len(meta["mem"]))
+        mem = ks.encrypt_words(meta["mem"], WIDTH, 940).reshape(1, -1, 631)
+        res, st, wall, dev, br = run(dag, mem)
+        bits = ks.decrypt(res.reshape(-1, 631))
+        words = bits[:8 * WIDTH].reshape(8, WIDTH).astype(np.int64)
+        vals = [int((w << np.arange(WIDTH)).sum()) for w in words]
+        ok = vals == meta["regs"] and list(bits[8 * WIDTH:]) == meta["nzcv"]
+        out["config5_program"] = {"instructions": len(prog), "recorded_gates": st["bootstrapped"],
+                                  "executed_gates": st["executed"],
+                                  "dataflow_levels": st["last_flush_levels"],
+                                  "latency_s": wall, "device_ms": dev,
+                                  "instructions_per_s": len(prog) / wall, "correct": bool(ok)}
+        # the same program on the reference's own Machine through the drop-in
+        # (cryptovm::GpuBackend, demand-driven): record + evaluate + decrypt
+        t = time.perf_counter()
+        regs, nzcv, st2, _ = refshim.run_program_gpu(ctx, ks, prog, meta["mem"])
+        wall2 = time.perf_counter() - t
+        out["config5_reference_machine"] = {
+            "latency_s": wall2, "executed_gates": st2["executed"],
+            "recorded_gates": st2["bootstrapped"],
+            "correct": bool([int(r) for r in regs] == meta["regs"]
+                            and list(nzcv) == meta["nzcv"])}
     ctx.set_profiling(False)
     return out
 
 
 # ------------------------------------------------------------------ ours --
+def pinned_copy(a):
+    try:
+        import torch
+        p = torch.empty(a.shape, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        p[...] = a
+        return p
+    except Exception:
+        return a
+
+
 def run_ours(args):
     import paper_2101_03403_b200 as P
     ws, rank, local = dist_env()
@@ -323,27 +415,28 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        import torch
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     ks = P.KeySet(KEY_SEED)
     ctx = P.Context(local)
     ctx.upload_keyset(ks)
+    add16 = load_dag("add", WIDTH)
+    assert add16.bootstrapped() == GATES_PER_ADD and add16.n_inputs == 2 * WIDTH
     av, bv = workload_operands(rank)
-    a_lwe = ks.encrypt_words(av, WIDTH, 100 + rank)
-    b_lwe = ks.encrypt_words(bv, WIDTH, 200 + rank)
-    # pinned host copies for the e2e leg
-    try:
-        import torch
-        pa = torch.empty(a_lwe.shape, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-        pb = torch.empty(b_lwe.shape, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-        pa[...] = a_lwe
-        pb[...] = b_lwe
-    except Exception:
-        pa, pb = a_lwe, b_lwe
+    lwe = operand_lwe(ks, "add", WIDTH, av, bv, 100 + 2 * rank)  # (256, 32, 631)
+    pin = pinned_copy(lwe)  # pinned host buffer for the e2e leg
 
-    # Record the 256 adders once; replay the levelised plan each step.
+    # Record the 256 adders once (replay of the reference's table); replay the
+    # levelised plan each step.
     bk = P.Backend(ctx)
-    ha = bk.import_lwe(a_lwe.reshape(-1, 631)).reshape(BATCH, WIDTH)
-    hb = bk.import_lwe(b_lwe.reshape(-1, 631)).reshape(BATCH, WIDTH)
-    outs = np.stack([bk.fu("add", ha[i], hb[i]) for i in range(BATCH)])
+    hin = bk.import_lwe(lwe.reshape(-1, 631)).reshape(BATCH, -1)
+    outs = np.stack([bk.replay_outputs(add16, hin[i]) for i in range(BATCH)])
     plan = bk.capture_plan()
     info = plan.info()
     assert info["gates"] == BATCH * GATES_PER_ADD and info["levels"] == 9, info
@@ -372,12 +465,7 @@ def run_ours(args):
     ctx.sync()
     barrier()
     kst = ctx.kernel_stats()
-    total_ms = sum(step_ms)
-    if dist:
-        import torch
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms))
     gates_step = info["gates"]
     boots_step = info["bootstraps"]
     value = ws * gates_step * args.steps / (total_ms * 1e-3)
@@ -392,30 +480,47 @@ def run_ours(args):
     for i in range(args.warmup + args.steps):
         barrier()
         t = time.perf_counter()
-        out, st = P.fu_batch(ctx, "add", WIDTH, pa, pb)
+        res, st = P.dag_batch(ctx, add16, pin)
         dt = time.perf_counter() - t
         if i >= args.warmup:
             e2e_times.append(dt)
-    vals = ks.decrypt_words(out.reshape(-1, 631), WIDTH + 1)
+    vals = ks.decrypt_words(res.reshape(-1, 631), WIDTH + 1)
     assert np.array_equal(vals, av + bv), "e2e produced wrong sums"
-    e2e_total = sum(e2e_times)
-    if dist:
-        import torch
-        t = torch.tensor([e2e_total], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    # cvm_fu_batch evaluates only the exported outputs' cone (dead-gate
+    e2e_total = max_over_ranks(sum(e2e_times))
+    # cvm_dag_batch evaluates only the exported outputs' cone (dead-gate
     # elimination: 180 of an ADD16's 195 gates feed sum + carry), so its rate
     # counts the gates it actually bootstraps; ADD16/s is the application rate.
     e2e_gates = int(st["executed"])
     e2e_value = ws * e2e_gates * args.steps / e2e_total
     e2e_add16 = ws * BATCH * args.steps / e2e_total
 
+    # the reference's own API through the drop-in shim: Word::encrypt, alu::add
+    # on cryptovm::GpuBackend, one evaluate, decrypt_word per result
+    ref_api = None
+    sys.path.insert(0, os.path.join(REPO, "integration"))
+    import refshim
+    if refshim.available():
+        times = []
+        for i in range(1 + min(args.steps, 3)):
+            barrier()
+            t = time.perf_counter()
+            sums, carries, st_r = refshim.add_batch_gpu(ctx, ks, av, bv, WIDTH)
+            if i:
+                times.append(time.perf_counter() - t)
+        ok = np.array_equal(sums + (carries.astype(np.uint64) << WIDTH), av + bv)
+        tot = max_over_ranks(sum(times))
+        ref_api = {"value": ws * st_r["executed"] * len(times) / tot,
+                   "unit": "bootstrapped gates/s", "add16_ops_per_s": ws * BATCH * len(times) / tot,
+                   "ms_per_step": 1e3 * tot / len(times), "correct": bool(ok),
+                   "path": "reference Word::encrypt + alu::add on cryptovm::GpuBackend "
+                           "(integration/), evaluate, decrypt_word per result; host "
+                           "encryption / decryption inside the timed region"}
+
     # batch-1 latency of one ADD16 (9 levels of <= 32 gates)
     lat = None
     if rank == 0:
         b1 = P.Backend(ctx)
-        o1 = b1.fu("add", b1.import_lwe(a_lwe[0]), b1.import_lwe(b_lwe[0]))
+        o1 = b1.replay_outputs(add16, b1.import_lwe(lwe[0]))
         p1 = b1.capture_plan()
         p1.run(ctx)
         ctx.sync()
@@ -427,17 +532,20 @@ def run_ours(args):
         assert s1 == av[0] + bv[0], "batch-1 adder produced a wrong sum"
 
     if rank != 0:
+        if dist:
+            dist.destroy_process_group()
         return 0
-    extras = extra_configs(P, ctx, ks) if (ws == 1 and not args.no_extras) else None
+    extras = extra_configs(P, ctx, ks, fp64_peak) if (ws == 1 and not args.no_extras) else None
     cpu = cpu_baseline() if (ws == 1 and not args.no_cpu) else None
     # DRAM bytes per blind-rotation launch of this workload, from the committed
     # ncu capture of the same command (profiles/ncu_blind_rotate.json)
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(REPO, "profiles", "ncu_blind_rotate.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            traffic = pj[pj.get("dominant", "blind_rotate_v3")]["avg_dram_bytes_per_launch"]
+            traffic = pj[pj.get("dominant", "blind_rotate_v4")]["avg_dram_bytes_per_launch"]
+            traffic_src = pj.get("source")
         except (KeyError, ValueError):
             traffic = None
     line = {
@@ -449,19 +557,23 @@ def run_ours(args):
                                "9 dataflow levels), n=630 N=1024 l=3 Bg=2^7 t=8 base 4",
                    "global_batch": BATCH * ws, "gates_per_step": gates_step * ws,
                    "parallelism": f"dp{ws} (independent adders per GPU)",
+                   "circuit": add16.source,
                    "l2": "flushed (256 MB memset) before every timed step"},
         "add16_ops_per_s": value / GATES_PER_ADD,
         "add16_batch_latency_ms": total_ms / args.steps,
         "add16_latency_batch1_ms": lat,
         "e2e": {"value": e2e_value, "unit": "bootstrapped gates/s",
-                "h2d_bytes_per_step": int(pa.nbytes + pb.nbytes),
+                "h2d_bytes_per_step": int(pin.nbytes),
                 "d2h_bytes_per_step": int(BATCH * (WIDTH + 1) * 631 * 4),
                 "gates_executed_per_step": e2e_gates * ws,
-                "add16_ops_per_s": e2e_add16},
-        "roofline": {"bound": "fp64", "kernel": "blind_rotate_kernel_v4 (+ v3/wide remainders)",
+                "add16_ops_per_s": e2e_add16,
+                "call": "cvm_dag_batch (C ABI), pinned host buffers",
+                "reference_api": ref_api},
+        "roofline": {"bound": "fp64", "kernel": "blind rotation (v4 waves + remainder kernels)",
                      "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per blind_rotate launch (ncu)",
+                     "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": 61_931_520 + (2524 + 4112) * boots_step
                      / max(1.0, kst["br_launches"] / args.steps),
                      "peak_source": "DFMA peak measured live in bench.py (cvm_ctx_fp64_peak); "

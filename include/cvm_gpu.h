@@ -255,59 +255,48 @@ CVM_API int cvm_backend_nodes(const cvm_backend* b, uint64_t first, uint64_t cou
                               int64_t* rows /* count x 7 */);
 
 /* ------------------------------------------------------------------------
- * Functional units (reference alu.hpp:68-136), emitting gates into a backend.
- * Words are arrays of `width` handles, LSB first (word.hpp:28-57).
+ * Recorded circuits.  The reference's functional units (alu.hpp:68-136) and
+ * emulator (emulator.hpp:87-133) stay on the reference side of the boundary:
+ * they record their gates once through cryptovm::Backend (the shim in
+ * integration/ records into a SimBackend), and the recorded
+ * table -- the reference GateDag's node list (DagNode, dag.hpp:33-42, ids
+ * 1-based in creation order as GateDag::append assigns them, dag.cpp:57-73) --
+ * is handed to the device here.  The reference DAG does not store a
+ * CONSTANT's value; the recorder adds it.
  * ---------------------------------------------------------------------- */
-typedef enum cvm_fu_op {
-  CVM_FU_ADD = 0,       /* alu::add               out: width + carry      */
-  CVM_FU_ADD_CIN = 1,   /* alu::add(carry_in = c[0])                      */
-  CVM_FU_SUB = 2,       /* alu::sub               out: width + carry      */
-  CVM_FU_ADDSUB = 3,    /* alu::add_sub_select(subtract = c[0])           */
-  CVM_FU_CMP = 4,       /* SUBS/CMP: sub + flags  out: width + N,Z,C,V    */
-  CVM_FU_AND = 5, CVM_FU_ORR = 6, CVM_FU_EOR = 7, CVM_FU_ORN = 8,
-  CVM_FU_LSL = 9, CVM_FU_LSR = 10, CVM_FU_ASR = 11, /* shift_reg by word b */
-  CVM_FU_UMUL = 12,     /* alu::mul_unsigned      out: 2*width            */
-  CVM_FU_SMUL = 13,     /* alu::mul_signed        out: 2*width            */
-  CVM_FU_UDIV = 14,     /* alu::div_unsigned (Widened) out: width         */
-  CVM_FU_UDIV_EXACT = 15,
-  CVM_FU_MUL_LO = 16    /* MUL as the emulator issues it: mul_unsigned, low
-                           half kept (emulator.cpp:271-285)  out: width   */
-} cvm_fu_op;
-CVM_API int cvm_fu_out_width(uint32_t op, uint32_t width);
-CVM_API int cvm_fu_apply(cvm_backend* b, uint32_t op, uint32_t width,
-                         const cvm_handle* a, const cvm_handle* bw,
-                         const cvm_handle* c, cvm_handle* out);
+typedef struct cvm_dag_node {
+  uint8_t kind;     /* cvm_gate_kind (DagNode::kind)                       */
+  uint8_t input;    /* 1: an encrypted input entering the session          */
+                    /*    (DagNode::input: encrypt_bit / import_bit)       */
+  uint8_t value;    /* CONSTANT: the constant bit                          */
+  uint8_t ndeps;    /* DagNode::dep_count: 0 (CONSTANT, input), 1 (NOT,    */
+                    /*    COPY), 2 (binary gates), 3 (MUX: sel, t, f)      */
+  uint32_t pad;
+  uint64_t dep[3];  /* DagNode::dep: ids of earlier nodes                  */
+} cvm_dag_node;
 
-/* Batched FU evaluation through the public path (host buffers in and out):
- * `batch` independent instances; operands a, b (and c for ADD_CIN/ADDSUB) are
- * ciphertexts batch x width x 631 u32 (c: batch x 631); results batch x
- * out_width x 631.  Records the circuits on a fresh backend, flushes the
- * levelised DAG through the device, downloads the outputs. */
-CVM_API int cvm_fu_batch(cvm_ctx* ctx, uint32_t op, uint32_t width, uint64_t batch,
-                         const uint32_t* a_lwe, const uint32_t* b_lwe,
-                         const uint32_t* c_lwe, uint32_t* out_lwe,
-                         cvm_backend_stats* stats);
+/* Re-issue a recorded table as Backend calls on `b`: input nodes take the
+ * handles `inputs` in node order (n_inputs must equal the table's input
+ * count), every other node becomes the gate call it records.  handles[i]
+ * receives node i+1's handle (n_nodes entries).  Lazy like every gate call. */
+CVM_API int cvm_backend_replay_dag(cvm_backend* b, const cvm_dag_node* nodes,
+                                   uint64_t n_nodes, const cvm_handle* inputs,
+                                   uint64_t n_inputs, cvm_handle* handles);
+/* Evaluate the cone of influence of `count` handles now (one flush), so the
+ * key owner's later bit-by-bit decryptions (word.cpp:70-77) only download. */
+CVM_API int cvm_backend_evaluate(cvm_backend* b, size_t count, const cvm_handle* hs);
 
-/* ------------------------------------------------------------------------
- * Emulator (reference Machine, emulator.hpp:87-133) for straight-line
- * programs: LOAD/STORE/MOV/ADD(S)/SUB(S)/MUL(S)/SMUL(S)/UDIV/LLS/LRS/ARS/AND/
- * OR/XOR/ORN/NOT/BFC/BFI/RBIT/REV/CMP/HALT (register or immediate operands;
- * B is rejected: it needs the key owner's branch oracle); fence after every
- * instruction is recorded but scheduling follows dataflow.
- * ---------------------------------------------------------------------- */
-typedef struct cvm_insn {
-  uint32_t op;        /* cryptovm::Opcode enumerator (isa.hpp:27-55)      */
-  int32_t rd, rn, rm; /* -1 = absent                                     */
-  int64_t imm;        /* -1 = absent                                     */
-  int64_t imm2;       /* BFC/BFI field width, -1 = absent                */
-  int32_t sets_flags;
-  int32_t pad;
-} cvm_insn;
-CVM_API int cvm_machine_run(cvm_backend* b, uint32_t word_size,
-                            uint32_t register_count, const cvm_handle* memory,
-                            uint32_t memory_words, const cvm_insn* program,
-                            uint32_t count, cvm_handle* regs_out,
-                            cvm_handle* nzcv_out);
+/* `batch` independent instances of one recorded circuit through the public
+ * path with host buffers: in_lwe is batch x n_inputs x 631 u32 (n_inputs =
+ * the table's input count), out_lwe batch x n_outputs x 631 (outputs: node
+ * ids).  The instances are recorded on a fresh backend, only the outputs'
+ * cone is evaluated (dead gates never run), levelised launches fill the
+ * GPU, results are downloaded; the call's scratch slots are returned.  The
+ * element counts of both buffers are checked against the table. */
+CVM_API int cvm_dag_batch(cvm_ctx* ctx, const cvm_dag_node* nodes, uint64_t n_nodes,
+                          const uint64_t* outputs, uint64_t n_outputs, uint64_t batch,
+                          const uint32_t* in_lwe, uint64_t in_words, uint32_t* out_lwe,
+                          uint64_t out_words, cvm_backend_stats* stats);
 
 #ifdef __cplusplus
 }

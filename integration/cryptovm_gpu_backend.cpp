@@ -19,12 +19,11 @@ void check(int rc, const char* what) {
 }  // namespace
 
 GpuBackend::GpuBackend(cvm_ctx* ctx, const cvm_keyset* owner, bool verify,
-                       std::uint64_t enc_seed)
+                       std::uint64_t enc_seed, bool flush_all)
     : owner_(owner), verify_(verify) {
   check(cvm_backend_create(ctx, owner, enc_seed, &gpu_), "cvm_backend_create");
-  // The reference decrypts words bit by bit (word.cpp:70-77): evaluate all
-  // pending gates at the first decrypt instead of one cone per bit.
-  check(cvm_backend_set_flush_policy(gpu_, CVM_FLUSH_ALL), "set_flush_policy");
+  check(cvm_backend_set_flush_policy(gpu_, flush_all ? CVM_FLUSH_ALL : CVM_FLUSH_CONE),
+        "set_flush_policy");
   map_.push_back(0);  // node id 0 is the invalid handle
 }
 
@@ -144,6 +143,14 @@ void GpuBackend::fence() {
 void GpuBackend::flush() {
   std::lock_guard<std::mutex> lock(mu_);
   check(cvm_backend_flush(gpu_), "flush");
+}
+
+void GpuBackend::evaluate(const std::vector<BitHandle>& bits) {
+  std::lock_guard<std::mutex> lock(mu_);
+  std::vector<cvm_handle> hs;
+  hs.reserve(bits.size());
+  for (const BitHandle& b : bits) hs.push_back(mapped(b, "evaluate"));
+  check(cvm_backend_evaluate(gpu_, hs.size(), hs.data()), "evaluate");
 }
 
 cvm_backend_stats GpuBackend::stats() const {

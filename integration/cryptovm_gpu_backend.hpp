@@ -18,6 +18,7 @@
 
 #include "cryptovm/gates.hpp"
 #include "cryptovm/sim_backend.hpp"
+#include "cryptovm/word.hpp"
 #include "cvm_gpu.h"
 
 namespace cryptovm {
@@ -26,8 +27,17 @@ class GpuBackend final : public Backend {
  public:
   // `ctx` must already hold the cloud keys (cvm_upload_keyset); `owner` is the
   // key owner's keyset used by encrypt_bit / decrypt_bit.
+  //
+  // Evaluation is demand-driven: a decrypt_bit / export_bit evaluates only the
+  // cone of influence of that bit, so gates whose results are never read (the
+  // high half of the emulator's MUL product, overwritten registers, replaced
+  // flags) never run.  The reference decrypts words bit by bit
+  // (word.cpp:70-77); a caller that knows which bits it will read next calls
+  // evaluate() on all of them first -- one flush, one batch of launches --
+  // and the decryptions after it only download.  flush_all = true restores
+  // "evaluate everything pending at the first decrypt".
   GpuBackend(cvm_ctx* ctx, const cvm_keyset* owner, bool verify = false,
-             std::uint64_t enc_seed = 1);
+             std::uint64_t enc_seed = 1, bool flush_all = false);
   ~GpuBackend() override;
   GpuBackend(const GpuBackend&) = delete;
   GpuBackend& operator=(const GpuBackend&) = delete;
@@ -48,6 +58,9 @@ class GpuBackend final : public Backend {
 
   // Evaluate everything recorded so far (one batched launch pair per level).
   void flush();
+  // Evaluate the cone of influence of `bits` now (one flush).
+  void evaluate(const std::vector<BitHandle>& bits);
+  void evaluate(const Word& word) { evaluate(word.bits()); }
   const GateDag& dag() const { return shadow_.dag(); }
   cvm_backend_stats stats() const;
   std::uint64_t mismatches() const { return mismatches_; }

@@ -9,7 +9,7 @@
 //   N <kind> <input> <ndeps> <d0> <d1> <d2> <const>  one line per DAG node,
 //                                          id = line index+1
 //   OUT <id> ...                            output node ids (LSB first)
-//   VEC <op> <width> <a> <b> <c> <result>   seeded cleartext vectors
+//   VEC <op> <width> <a> <b> <c> <result>   seeded / fixed cleartext vectors
 //   PROG <seed> ...                         config-5 program + final state
 #include <cstdint>
 #include <cstdio>
@@ -298,7 +298,7 @@ void cmd_program(std::uint64_t seed, int count) {
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr,
-                 "usage: ref_golden dag OP W | vec OP W SEED COUNT | exh OP W "
+                 "usage: ref_golden dag OP W | vec OP W SEED COUNT | exh OP W | one OP W A B C "
                  "| prog SEED COUNT\n");
     return 2;
   }
@@ -308,6 +308,18 @@ int main(int argc, char** argv) {
   } else if (cmd == "vec" && argc == 6) {
     cmd_vectors(argv[2], static_cast<unsigned>(std::atoi(argv[3])),
                 std::strtoull(argv[4], nullptr, 10), std::atoi(argv[5]), false);
+  } else if (cmd == "one" && argc == 7) {
+    // one fixed example: ref_golden one OP W A B C
+    const std::string op = argv[2];
+    const unsigned w = static_cast<unsigned>(std::atoi(argv[3]));
+    SimBackend bk;
+    Word a = Word::encrypt(bk, std::strtoull(argv[4], nullptr, 10), w);
+    Word b = Word::encrypt(bk, std::strtoull(argv[5], nullptr, 10), w);
+    BitHandle c = uses_c(op) ? bk.encrypt_bit(std::atoi(argv[6]) != 0) : BitHandle{};
+    std::vector<BitHandle> out = build(bk, op, a, b, c);
+    std::printf("VEC %s %u %s %s %s ", op.c_str(), w, argv[4], argv[5], argv[6]);
+    for (const BitHandle& h : out) std::printf("%d", bk.decrypt_bit(h) ? 1 : 0);
+    std::printf("\n");
   } else if (cmd == "exh" && argc == 4) {
     cmd_vectors(argv[2], static_cast<unsigned>(std::atoi(argv[3])), 0, 0, true);
   } else if (cmd == "prog" && argc == 4) {

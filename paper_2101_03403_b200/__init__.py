@@ -5,5 +5,5 @@ C ABI in ``include/cvm_gpu.h``); this package is a thin ctypes front end.
 """
 from ._native import (CvmDeviceError, CvmError, CvmInputError, CvmStateError,  # noqa: F401
                       LWE_WORDS, LIB_PATH)
-from .api import (FU, FU_OPS, KIND, OPCODE, Backend, Context, KeySet,  # noqa: F401
-                  fu_batch)
+from .api import (DAG_DTYPE, KIND, Backend, Context, Dag, KeySet,  # noqa: F401
+                  dag_batch)

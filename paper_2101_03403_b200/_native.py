@@ -62,10 +62,12 @@ class BackendStats(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-class Insn(ctypes.Structure):
-    _fields_ = [("op", ctypes.c_uint32), ("rd", ctypes.c_int32), ("rn", ctypes.c_int32),
-                ("rm", ctypes.c_int32), ("imm", ctypes.c_int64), ("imm2", ctypes.c_int64),
-                ("sets_flags", ctypes.c_int32), ("pad", ctypes.c_int32)]
+class DagNode(ctypes.Structure):
+    """cvm_dag_node: one node of a recorded circuit (the reference DagNode)."""
+    _fields_ = [("kind", ctypes.c_uint8), ("input", ctypes.c_uint8), ("value", ctypes.c_uint8),
+                ("ndeps", ctypes.c_uint8), ("pad", ctypes.c_uint32),
+                ("dep", ctypes.c_uint64 * 3)]
+
 
 
 _p = ctypes.c_void_p
@@ -136,11 +138,10 @@ _SIGS = {
     "cvm_backend_handle_slot": (_i, [_p, _u64, ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_uint32)]),
-    "cvm_fu_out_width":(_i, [_u32, _u32]),
-    "cvm_fu_apply": (_i, [_p, _u32, _u32, _p, _p, _p, _p]),
-    "cvm_fu_batch": (_i, [_p, _u32, _u32, _u64, _p, _p, _p, _p,
-                          ctypes.POINTER(BackendStats)]),
-    "cvm_machine_run": (_i, [_p, _u32, _u32, _p, _u32, _p, _u32, _p, _p]),
+    "cvm_backend_replay_dag": (_i, [_p, _p, _u64, _p, _u64, _p]),
+    "cvm_backend_evaluate": (_i, [_p, ctypes.c_size_t, _p]),
+    "cvm_dag_batch": (_i, [_p, _p, _u64, _p, _u64, _u64, _p, _u64, _p, _u64,
+                           ctypes.POINTER(BackendStats)]),
 }
 
 EXPORTED = tuple(_SIGS)

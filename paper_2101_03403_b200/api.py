@@ -1,7 +1,10 @@
 """Python front end of the B200 backend (thin; the product is libcvm_b200.so).
 
-Names follow the reference interface (cryptovm::Backend, gates.hpp:109-132;
-alu.hpp; Machine, emulator.hpp) so tests read like the reference's own.
+Names follow the reference interface (cryptovm::Backend, gates.hpp:109-132) so
+tests read like the reference's own.  Circuits (the reference's functional
+units and emulator) are not re-implemented here: they arrive as recorded gate
+tables (`Dag`, the reference GateDag's node list) and are replayed on the
+device (`Backend.replay`, `dag_batch`).
 """
 import ctypes
 
@@ -14,14 +17,51 @@ GATE_KINDS = ["CONSTANT", "NOT", "COPY", "NAND", "AND", "OR", "XOR", "XNOR", "NO
               "ANDNY", "ANDYN", "ORNY", "ORYN", "MUX"]
 KIND = {n: i for i, n in enumerate(GATE_KINDS)}
 
-FU_OPS = ["add", "add_cin", "sub", "addsub", "cmp", "and", "orr", "eor", "orn", "lsl",
-          "lsr", "asr", "umul", "smul", "udiv", "udiv_exact", "mul_lo"]
-FU = {n: i for i, n in enumerate(FU_OPS)}
+# cvm_dag_node (include/cvm_gpu.h): 32 bytes per node
+DAG_DTYPE = np.dtype([("kind", "u1"), ("input", "u1"), ("value", "u1"), ("ndeps", "u1"),
+                      ("pad", "<u4"), ("dep", "<u8", (3,))])
+assert DAG_DTYPE.itemsize == ctypes.sizeof(N.DagNode)
 
-OPCODES = ["LOAD", "STORE", "MOV", "ADD", "ADDS", "SUB", "SUBS", "MUL", "MULS", "SMUL",
-           "SMULS", "UDIV", "LLS", "LRS", "ARS", "AND", "OR", "XOR", "ORN", "NOT", "BFC",
-           "BFI", "RBIT", "REV", "CMP", "B", "HALT"]
-OPCODE = {n: i for i, n in enumerate(OPCODES)}
+
+class Dag:
+    """A recorded circuit: the reference GateDag's nodes (dag.hpp:33-42, ids
+    1-based in creation order) plus each CONSTANT's value, and the ids of its
+    output bits (LSB first).  Inputs are the input nodes in id order."""
+
+    def __init__(self, nodes, outputs, name=""):
+        self.nodes = np.ascontiguousarray(nodes, dtype=DAG_DTYPE)
+        self.outputs = np.ascontiguousarray(outputs, dtype=np.uint64)
+        self.name = name
+
+    @classmethod
+    def from_rows(cls, rows, outputs, name=""):
+        """rows: (n, 7) ints [kind, input, ndeps, d0, d1, d2, const_value] -- the
+        oracle / golden-fixture layout."""
+        rows = np.asarray(rows, dtype=np.int64).reshape(-1, 7)
+        nodes = np.zeros(len(rows), DAG_DTYPE)
+        nodes["kind"], nodes["input"], nodes["ndeps"] = rows[:, 0], rows[:, 1], rows[:, 2]
+        nodes["dep"] = rows[:, 3:6]
+        nodes["value"] = rows[:, 6]
+        return cls(nodes, outputs, name)
+
+    def rows(self):
+        r = np.zeros((len(self.nodes), 7), np.int64)
+        r[:, 0], r[:, 1], r[:, 2] = self.nodes["kind"], self.nodes["input"], self.nodes["ndeps"]
+        r[:, 3:6] = self.nodes["dep"]
+        r[:, 6] = self.nodes["value"]
+        return r
+
+    @property
+    def n_inputs(self):
+        return int(self.nodes["input"].sum())
+
+    @property
+    def n_nodes(self):
+        return len(self.nodes)
+
+    def bootstrapped(self):
+        k = self.nodes["kind"][self.nodes["input"] == 0]
+        return int((k >= KIND["NAND"]).sum())
 
 
 def _vp(a):
@@ -297,19 +337,23 @@ class Backend:
         check(lib.cvm_backend_nodes(self._h, 0, n.value, _vp(rows)))
         return rows
 
-    # -- functional units (alu.hpp) --
-    def fu(self, op, a, b, c=0):
-        a = np.ascontiguousarray(a, dtype=np.uint64)
-        b = np.ascontiguousarray(b, dtype=np.uint64)
-        w = len(a)
-        opi = FU[op] if isinstance(op, str) else op
-        ow = lib.cvm_fu_out_width(opi, w)
-        if ow < 0:
-            raise N.CvmInputError(f"unknown op {op}")
-        out = np.zeros(ow, np.uint64)
-        cc = np.array([c], np.uint64)
-        check(lib.cvm_fu_apply(self._h, opi, w, _vp(a), _vp(b), _vp(cc), _vp(out)))
+    # -- recorded circuits --
+    def replay(self, dag, inputs):
+        """Re-issue a recorded circuit on this backend; returns the handle of
+        every node (index = node id - 1)."""
+        inputs = np.ascontiguousarray(inputs, dtype=np.uint64).ravel()
+        out = np.zeros(dag.n_nodes, np.uint64)
+        check(lib.cvm_backend_replay_dag(self._h, dag.nodes.ctypes.data, dag.n_nodes,
+                                         _vp(inputs), len(inputs), _vp(out)))
         return out
+
+    def replay_outputs(self, dag, inputs):
+        return self.replay(dag, inputs)[dag.outputs.astype(np.int64) - 1]
+
+    def evaluate(self, hs):
+        """Evaluate the cone of `hs` now (one flush)."""
+        hs = np.ascontiguousarray(hs, dtype=np.uint64).ravel()
+        check(lib.cvm_backend_evaluate(self._h, len(hs), _vp(hs)))
 
     def encrypt_word(self, value, width):
         return np.array([self.encrypt_bit((value >> i) & 1) for i in range(width)], np.uint64)
@@ -317,23 +361,6 @@ class Backend:
     def decrypt_word(self, hs):
         bits = self.decrypt_bits(hs).astype(np.uint64)
         return int((bits << np.arange(len(bits), dtype=np.uint64)).sum())
-
-    def machine_run(self, program, memory, word_size=16, register_count=8):
-        """program: list of (op, rd, rn, rm, imm, sets_flags[, imm2]); memory:
-        list of handle arrays (width each).  Returns (regs handles, nzcv handles)."""
-        arr = (N.Insn * len(program))()
-        for x, ins in zip(arr, program):
-            op, rd, rn, rm, imm, sf = ins[:6]
-            x.op = OPCODE[op] if isinstance(op, str) else op
-            x.rd, x.rn, x.rm, x.imm, x.sets_flags = rd, rn, rm, imm, sf
-            x.imm2 = ins[6] if len(ins) > 6 else -1
-        mem = np.ascontiguousarray(np.array(memory, dtype=np.uint64).reshape(-1)) \
-            if len(memory) else np.zeros(1, np.uint64)
-        regs = np.zeros(register_count * word_size, np.uint64)
-        nzcv = np.zeros(4, np.uint64)
-        check(lib.cvm_machine_run(self._h, word_size, register_count, _vp(mem), len(memory),
-                                  arr, len(program), _vp(regs), _vp(nzcv)))
-        return regs.reshape(register_count, word_size), nzcv
 
 
 class Plan:
@@ -358,16 +385,19 @@ class Plan:
         return {"levels": lv.value, "gates": g.value, "bootstraps": b.value}
 
 
-def fu_batch(ctx, op, width, a_lwe, b_lwe, c_lwe=None):
-    """Batched functional unit through the public path (host buffers)."""
-    opi = FU[op] if isinstance(op, str) else op
-    a = _u32(a_lwe)
-    b = _u32(b_lwe)
-    batch = a.size // (width * N.LWE_WORDS)
-    c = _u32(c_lwe) if c_lwe is not None else None
-    ow = lib.cvm_fu_out_width(opi, width)
-    out = np.empty((batch, ow, N.LWE_WORDS), np.uint32)
+def dag_batch(ctx, dag, in_lwe):
+    """`batch` independent instances of a recorded circuit through the public
+    C-ABI call cvm_dag_batch with host buffers: in_lwe (batch, n_inputs, 631)
+    -> (batch, n_outputs, 631) ciphertexts, backend stats."""
+    a = _u32(in_lwe)
+    per = dag.n_inputs * N.LWE_WORDS
+    if per == 0 or a.size % per:
+        raise N.CvmInputError(f"in_lwe has {a.size} words, not a multiple of "
+                              f"{dag.n_inputs} inputs x {N.LWE_WORDS}")
+    batch = a.size // per
+    out = np.empty((batch, len(dag.outputs), N.LWE_WORDS), np.uint32)
     st = N.BackendStats()
-    check(lib.cvm_fu_batch(ctx.handle, opi, width, batch, _vp(a), _vp(b), _vp(c), _vp(out),
-                           ctypes.byref(st)))
+    check(lib.cvm_dag_batch(ctx.handle, dag.nodes.ctypes.data, dag.n_nodes,
+                            _vp(dag.outputs), len(dag.outputs), batch, _vp(a), a.size,
+                            _vp(out), out.size, ctypes.byref(st)))
     return out, st.as_dict()

@@ -31,7 +31,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xptxas", "-v",
 CXX_FLAGS = ["-std=c++20"] + HOST_FLAGS + ["-I/usr/local/cuda/include"]
 
 SOURCES = ["blind_rotate.cu", "blind_rotate_v4.cu", "key_switch.cu", "device_misc.cu", "context.cu", "keys.cpp",
-           "backend.cpp", "schedule.cpp", "clear_backend.cpp", "alu.cpp", "machine.cpp", "capi.cpp"]
+           "backend.cpp", "schedule.cpp", "clear_backend.cpp", "dag.cpp", "capi.cpp"]
 HEADERS = ["tfhe_params.h", "fft512.cuh", "fft512w.cuh", "br_common.cuh", "schedule.hpp", "sm100.cuh", "kernels.cuh", "cvm_internal.hpp"]
 
 

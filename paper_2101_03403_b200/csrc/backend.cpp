@@ -372,6 +372,15 @@ void GpuBackend::run(const std::vector<Bit>& ids) {
 
 void GpuBackend::flush() {
   std::lock_guard<std::mutex> lock(mu_);
+  flush_locked();
+}
+
+void GpuBackend::flush_locked() {
+  for (Bit id : pending_) {
+    const Node& n = nodes_[id - 1];
+    for (int d = 0; d < n.ndeps; ++d)
+      if (nodes_[n.dep[d] - 1].level == 0) check_captured(nodes_[n.dep[d] - 1]);
+  }
   if (pending_.empty()) {
     stage_uploads();
     return;
@@ -380,13 +389,28 @@ void GpuBackend::flush() {
   run(all);
 }
 
+// A handle whose value a captured plan produces is readable only once that
+// plan has run (capture marks its gates resident up front).
+void GpuBackend::check_captured(const Node& n) const {
+  if (n.plan && !plans_[n.plan - 1]->load())
+    throw StateError("handle is produced by a captured plan that has not run yet");
+}
+
 // Evaluates the cone of influence of `hs` only.
 void GpuBackend::flush_for(size_t count, const Bit* hs) {
   std::lock_guard<std::mutex> lock(mu_);
+  for (size_t i = 0; i < count; ++i) node(hs[i], "evaluate");
+  flush_for_locked(count, hs);
+}
+
+void GpuBackend::flush_for_locked(size_t count, const Bit* hs) {
   std::vector<Bit> need, stack;
   std::vector<uint8_t> seen;
-  for (size_t i = 0; i < count; ++i)
-    if (nodes_[hs[i] - 1].level != 0) stack.push_back(hs[i]);
+  for (size_t i = 0; i < count; ++i) {
+    const Node& n = nodes_[hs[i] - 1];
+    if (n.level != 0) stack.push_back(hs[i]);
+    else check_captured(n);
+  }
   if (stack.empty()) {
     stage_uploads();
     return;
@@ -396,7 +420,11 @@ void GpuBackend::flush_for(size_t count, const Bit* hs) {
     const Bit id = stack.back();
     stack.pop_back();
     const Node& n = nodes_[id - 1];
-    if (n.level == 0 || seen[id - first_pending_]) continue;
+    if (n.level == 0) {
+      check_captured(n);
+      continue;
+    }
+    if (seen[id - first_pending_]) continue;
     seen[id - first_pending_] = 1;
     if (is_gate(n.kind)) need.push_back(id);
     for (int d = 0; d < n.ndeps; ++d) stack.push_back(n.dep[d]);
@@ -406,6 +434,8 @@ void GpuBackend::flush_for(size_t count, const Bit* hs) {
 }
 
 // Moves every pending level into a replayable plan (uploads are enqueued now).
+// Its gates count as resident from here on, but reading one (export, decrypt,
+// or a flush of a gate built on it) throws StateError until the plan has run.
 Plan* GpuBackend::capture_plan() {
   std::lock_guard<std::mutex> lock(mu_);
   context_reserve(ctx_, context_slots_used(ctx_));
@@ -413,6 +443,9 @@ Plan* GpuBackend::capture_plan() {
   const std::vector<Bit> all = pending_;
   const auto lv = levels_of(all);
   Plan* p = context_make_plan(ctx_, lv);
+  p->ran = std::make_shared<std::atomic<bool>>(all.empty());
+  plans_.push_back(p->ran);
+  for (Bit id : all) nodes_[id - 1].plan = uint32_t(plans_.size());
   for (const auto& level : lv)
     stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, level.size());
   stats_.last_flush_levels = lv.size();
@@ -422,10 +455,15 @@ Plan* GpuBackend::capture_plan() {
 }
 
 void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
-  for (size_t i = 0; i < count; ++i) node(hs[i], "export");
-  if (cone_only_) flush_for(count, hs);
-  else flush();
   std::lock_guard<std::mutex> lock(mu_);
+  for (size_t i = 0; i < count; ++i) node(hs[i], "export");
+  if (cone_only_) {
+    flush_for_locked(count, hs);
+  } else {
+    for (size_t i = 0; i < count; ++i)
+      if (nodes_[hs[i] - 1].level == 0) check_captured(nodes_[hs[i] - 1]);
+    flush_locked();
+  }
   // One device gather of the requested slots (in request order) and one
   // download, then the linear forms (NOT / COPY / CONSTANT) applied on the host.
   std::vector<uint64_t> sl;

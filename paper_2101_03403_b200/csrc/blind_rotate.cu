@@ -914,7 +914,7 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
 template <int G, int S, bool kTwRec = false>
 static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(BrSmem2<G, S>));
   cudaError_t e = set_smem(blind_rotate_kernel_v2<G, S, kTwRec>, smem, configured);
   if (e != cudaSuccess) return e;
@@ -927,7 +927,7 @@ template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = fa
           bool kLast = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(BrSmem3<G, S>));
   auto* kern = blind_rotate_kernel_v3<G, S, kTmem, kTwRec, kHold, kLast>;
   cudaError_t e = set_smem(kern, smem, configured);
@@ -940,7 +940,7 @@ template <bool kTwRec = false>
 static cudaError_t launch_wide(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(WideSmem));
   cudaError_t e = set_smem(blind_rotate_wide_kernel<kTwRec>, smem, configured);
   if (e != cudaSuccess) return e;
@@ -953,7 +953,7 @@ template <bool kAsync = false>
 static cudaError_t launch_pair(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(PairSmem));
   cudaError_t e = set_smem(blind_rotate_pair_kernel<kAsync>, smem, configured);
   if (e != cudaSuccess) return e;

@@ -268,7 +268,7 @@ cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, c
 template <int S, bool kHold>
 static cudaError_t launch_v4(int warps, const BrJob* jobs, int count, const uint32_t* slab,
                              const c64* bkf4, const c64* tw4, uint32_t* xout, cudaStream_t s) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   auto* kern = blind_rotate_kernel_v4<S, kHold>;
   cudaError_t e = set_smem(kern, v4_smem_bytes<S>(kV4MaxWarps), configured);
   if (e != cudaSuccess) return e;

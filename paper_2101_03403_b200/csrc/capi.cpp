@@ -62,7 +62,6 @@ GateKind kind_of(uint32_t k) {
   return GateKind(k);
 }
 
-Word to_word(const cvm_handle* h, uint32_t w) { return Word(h, h + w); }
 
 }  // namespace
 
@@ -477,55 +476,56 @@ int cvm_backend_handle_slot(const cvm_backend* b, cvm_handle h, int64_t* slot, i
   });
 }
 
-// ----------------------------------------------------- functional units --
-int cvm_fu_out_width(uint32_t op, uint32_t width) { return fu_out_width(op, width); }
-
-int cvm_fu_apply(cvm_backend* b, uint32_t op, uint32_t width, const cvm_handle* a,
-                 const cvm_handle* bw, const cvm_handle* c, cvm_handle* out) {
+// --------------------------------------------------------------- circuits --
+int cvm_backend_replay_dag(cvm_backend* b, const cvm_dag_node* nodes, uint64_t n,
+                           const cvm_handle* inputs, uint64_t n_inputs, cvm_handle* handles) {
   return guard([&] {
     need(b, "backend");
-    need(a, "a");
-    need(bw, "b");
-    need(out, "out");
-    const int ow = fu_out_width(op, width);
-    if (ow < 0) throw InputError("unknown functional-unit op");
-    const bool uses_c = op == CVM_FU_ADD_CIN || op == CVM_FU_ADDSUB;
-    if (uses_c) need(c, "c");
-    Word r = fu_apply(*b->impl, op, to_word(a, width), to_word(bw, width), uses_c ? *c : 0);
-    std::memcpy(out, r.data(), r.size() * sizeof(Bit));
+    if (n_inputs) need(inputs, "inputs");
+    replay_dag(*b->impl, nodes, n, inputs, n_inputs, handles);
+  });
+}
+int cvm_backend_evaluate(cvm_backend* b, size_t n, const cvm_handle* hs) {
+  return guard([&] {
+    need(b, "backend");
+    if (n) need(hs, "handles");
+    if (b->gpu) b->gpu->flush_for(n, hs);
   });
 }
 
-int cvm_fu_batch(cvm_ctx* c, uint32_t op, uint32_t width, uint64_t batch, const uint32_t* a_lwe,
-                 const uint32_t* b_lwe, const uint32_t* c_lwe, uint32_t* out_lwe,
-                 cvm_backend_stats* stats) {
+int cvm_dag_batch(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_nodes,
+                  const uint64_t* outputs, uint64_t n_outputs, uint64_t batch,
+                  const uint32_t* in_lwe, uint64_t in_words, uint32_t* out_lwe,
+                  uint64_t out_words, cvm_backend_stats* stats) {
   return guard([&] {
     need(c, "ctx");
-    need(a_lwe, "a");
-    need(b_lwe, "b");
-    need(out_lwe, "out");
-    const int ow = fu_out_width(op, width);
-    if (ow < 0) throw InputError("unknown functional-unit op");
-    const bool uses_c = op == CVM_FU_ADD_CIN || op == CVM_FU_ADDSUB;
-    if (uses_c) need(c_lwe, "c");
+    uint64_t n_in = 0;
+    validate_dag(nodes, n_nodes, &n_in);
+    if (n_outputs) need(outputs, "outputs");
+    for (uint64_t o = 0; o < n_outputs; ++o)
+      if (outputs[o] == 0 || outputs[o] > n_nodes) throw InputError("output id out of range");
+    if (in_words != batch * n_in * kLweWords)
+      throw InputError("in_lwe holds " + std::to_string(in_words) + " words, the batch needs " +
+                       std::to_string(batch * n_in * kLweWords));
+    if (out_words != batch * n_outputs * kLweWords)
+      throw InputError("out_lwe holds " + std::to_string(out_words) + " words, the batch needs " +
+                       std::to_string(batch * n_outputs * kLweWords));
+    if (in_words) need(in_lwe, "in_lwe");
+    if (out_words) need(out_lwe, "out_lwe");
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     GpuBackend bk(c->ctx, nullptr, 0);
-    std::vector<Bit> ha(batch * width), hb(batch * width), hc(uses_c ? batch : 0);
+    std::vector<Bit> in(batch * n_in), handles(n_nodes), outs(batch * n_outputs);
     // Inputs are DMA'd straight from the caller's buffers; every path out of
     // this call synchronises the stream first, so they may be released after.
     auto t1 = t0, t2 = t0;
     try {
-      bk.import_lwe_direct(ha.size(), a_lwe, ha.data());
-      bk.import_lwe_direct(hb.size(), b_lwe, hb.data());
-      if (uses_c) bk.import_lwe_direct(hc.size(), c_lwe, hc.data());
+      bk.import_lwe_direct(in.size(), in_lwe, in.data());
       t1 = clk::now();
-      std::vector<Bit> outs;
-      outs.reserve(batch * size_t(ow));
       for (uint64_t i = 0; i < batch; ++i) {
-        Word r = fu_apply(bk, op, Word(&ha[i * width], &ha[i * width] + width),
-                          Word(&hb[i * width], &hb[i * width] + width), uses_c ? hc[i] : 0);
-        outs.insert(outs.end(), r.begin(), r.end());
+        replay_dag(bk, nodes, n_nodes, in.data() + i * n_in, n_in, handles.data());
+        for (uint64_t o = 0; o < n_outputs; ++o)
+          outs[i * n_outputs + o] = handles[outputs[o] - 1];
       }
       t2 = clk::now();
       bk.export_lwe(outs.size(), outs.data(), out_lwe);  // synchronises
@@ -535,37 +535,12 @@ int cvm_fu_batch(cvm_ctx* c, uint32_t op, uint32_t width, uint64_t batch, const 
       throw;
     }
     if (stats) *stats = bk.stats();
-    if (std::getenv("CVM_FU_TIMING")) {
+    if (std::getenv("CVM_DAG_TIMING")) {
       const auto ms = [](auto a, auto b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
       };
-      std::fprintf(stderr, "cvm_fu_batch: import %.2f ms, record %.2f ms, run+export %.2f ms\n",
+      std::fprintf(stderr, "cvm_dag_batch: import %.2f ms, record %.2f ms, run+export %.2f ms\n",
                    ms(t0, t1), ms(t1, t2), ms(t2, clk::now()));
-    }
-  });
-}
-
-// -------------------------------------------------------------- machine --
-int cvm_machine_run(cvm_backend* b, uint32_t word_size, uint32_t register_count,
-                    const cvm_handle* memory, uint32_t memory_words, const cvm_insn* program,
-                    uint32_t count, cvm_handle* regs_out, cvm_handle* nzcv_out) {
-  return guard([&] {
-    need(b, "backend");
-    if (count) need(program, "program");
-    std::vector<Word> mem;
-    for (uint32_t w = 0; w < memory_words; ++w)
-      mem.push_back(Word(memory + size_t(w) * word_size, memory + size_t(w + 1) * word_size));
-    std::vector<Word> regs;
-    alu::Flags f{};
-    machine_run(*b->impl, word_size, register_count, mem, program, count, &regs, &f);
-    if (regs_out)
-      for (size_t r = 0; r < regs.size(); ++r)
-        std::memcpy(regs_out + r * word_size, regs[r].data(), word_size * sizeof(Bit));
-    if (nzcv_out) {
-      nzcv_out[0] = f.n;
-      nzcv_out[1] = f.z;
-      nzcv_out[2] = f.c;
-      nzcv_out[3] = f.v;
     }
   });
 }

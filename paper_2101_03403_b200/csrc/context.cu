@@ -10,6 +10,7 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "cvm_internal.hpp"
@@ -543,14 +544,26 @@ class Context {
   std::vector<Prof> prof_;
   size_t prof_used_ = 0;
   cudaEvent_t ev_user_[2]{};
+
+ public:
+  // Serialises the context's stream, arenas, slab and counters between the
+  // backends (and raw level API callers) of several threads sharing it; each
+  // entry point below holds it for its whole call.  The slot
+  // allocator has its own lock (alloc_mu_).
+  std::recursive_mutex mu;
 };
 
 Context* context_create(int device) { return new Context(device); }
 void context_destroy(Context* c) { delete c; }
+using CtxLock = std::lock_guard<std::recursive_mutex>;
 void context_upload_keys(Context* c, const uint32_t* bk, const uint32_t* ksk) {
+  CtxLock l(c->mu);
   c->upload_keys(bk, ksk);
 }
-void context_reserve(Context* c, uint64_t n) { c->reserve(n); }
+void context_reserve(Context* c, uint64_t n) {
+  CtxLock l(c->mu);
+  c->reserve(n);
+}
 uint64_t context_capacity(const Context* c) { return c->capacity(); }
 uint64_t context_alloc_slots(Context* c, uint64_t n) { return c->alloc_slots(n); }
 uint64_t context_slots_used(const Context* c) { return c->slots_used(); }
@@ -558,33 +571,68 @@ bool context_release_slots(Context* c, uint64_t first, uint64_t end) {
   return c->release_slots(first, end);
 }
 void context_upload(Context* c, uint64_t slot, uint64_t count, const uint32_t* lwe) {
+  CtxLock l(c->mu);
   c->upload(slot, count, lwe);
 }
 void context_download(Context* c, uint64_t slot, uint64_t count, uint32_t* lwe) {
+  CtxLock l(c->mu);
   c->download(slot, count, lwe);
 }
 void context_gather_download(Context* c, const uint64_t* slots, uint64_t count,
                              uint32_t* lwe) {
+  CtxLock l(c->mu);
   c->gather_download(slots, count, lwe);
 }
-void context_submit_level(Context* c, const cvm_gate* g, uint64_t n) { c->submit_level(g, n); }
-void context_sync(Context* c) { c->sync(); }
+void context_submit_level(Context* c, const cvm_gate* g, uint64_t n) {
+  CtxLock l(c->mu);
+  c->submit_level(g, n);
+}
+void context_sync(Context* c) {
+  CtxLock l(c->mu);
+  c->sync();
+}
 Plan* context_make_plan(Context* c, const std::vector<std::vector<cvm_gate>>& levels) {
+  CtxLock l(c->mu);
   return c->make_plan(levels);
 }
-void context_run_plan(Context* c, Plan* p, bool graph) { c->run_plan(p, graph); }
+void context_run_plan(Context* c, Plan* p, bool graph) {
+  CtxLock l(c->mu);
+  c->run_plan(p, graph);
+  if (p->ran) p->ran->store(true);  // its results are stream-ordered before any read
+}
 Plan::~Plan() {
   if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
   cudaFree(dmem);
 }
 bool context_has_keys(const Context* c) { return c->has_keys(); }
-void context_set_profiling(Context* c, bool on) { c->profiling = on; }
-cvm_kernel_stats context_stats(Context* c) { return c->stats_; }
-void context_reset_stats(Context* c) { c->stats_ = cvm_kernel_stats{}; }
-void context_flush_l2(Context* c) { c->flush_l2(); }
-void context_event(Context* c, int which) { c->event(which); }
-double context_event_elapsed(Context* c) { return c->event_elapsed(); }
-double context_fp64_peak(Context* c, int reps) { return c->fp64_peak(reps); }
+void context_set_profiling(Context* c, bool on) {
+  CtxLock l(c->mu);
+  c->profiling = on;
+}
+cvm_kernel_stats context_stats(Context* c) {
+  CtxLock l(c->mu);
+  return c->stats_;
+}
+void context_reset_stats(Context* c) {
+  CtxLock l(c->mu);
+  c->stats_ = cvm_kernel_stats{};
+}
+void context_flush_l2(Context* c) {
+  CtxLock l(c->mu);
+  c->flush_l2();
+}
+void context_event(Context* c, int which) {
+  CtxLock l(c->mu);
+  c->event(which);
+}
+double context_event_elapsed(Context* c) {
+  CtxLock l(c->mu);
+  return c->event_elapsed();
+}
+double context_fp64_peak(Context* c, int reps) {
+  CtxLock l(c->mu);
+  return c->fp64_peak(reps);
+}
 int context_sm_count(const Context* c) { return c->sm_count(); }
 
 }  // namespace cvm

@@ -1,6 +1,8 @@
 // Internal C++ interfaces behind the C ABI (include/cvm_gpu.h).
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -57,6 +59,7 @@ struct Plan {
   const void* graph_slab = nullptr;
   const void* graph_xlwe = nullptr;
   const Context* owner = nullptr;  // the context whose slots and memory it uses
+  std::shared_ptr<std::atomic<bool>> ran;  // set by the first cvm_plan_run
 };
 Context* context_create(int device);
 void context_destroy(Context* c);
@@ -87,9 +90,8 @@ int context_sm_count(const Context* c);
 
 // --------------------------------------------------------------- backend --
 // Mirror of cryptovm::Backend (gates.hpp:109-132) with handles as dense node
-// ids (0 = invalid), so the functional units below read like the reference.
+// ids (0 = invalid).
 using Bit = uint64_t;
-using Word = std::vector<Bit>;
 
 enum class GateKind : uint8_t {
   Constant, Not, Copy, Nand, And, Or, Xor, Xnor, Nor, AndNY, AndYN, OrNY, OrYN, Mux
@@ -110,24 +112,6 @@ class Backend {
   virtual void fence() = 0;
 };
 
-inline Bit not_gate(Backend& b, Bit a) { return b.unary_gate(GateKind::Not, a); }
-inline Bit copy_gate(Backend& b, Bit a) { return b.unary_gate(GateKind::Copy, a); }
-inline Bit and_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::And, x, y); }
-inline Bit or_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Or, x, y); }
-inline Bit xor_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Xor, x, y); }
-inline Bit nand_gate(Backend& b, Bit x, Bit y) { return b.binary_gate(GateKind::Nand, x, y); }
-
-class Region {  // RegionScope (gates.hpp:158-170)
- public:
-  Region(Backend& b, std::string_view name) : b_(b) { b_.push_region(name); }
-  ~Region() { b_.pop_region(); }
-  Region(const Region&) = delete;
-  Region& operator=(const Region&) = delete;
-
- private:
-  Backend& b_;
-};
-
 // Node record (the reference DagNode, dag.hpp:33-42, minus cost/region).
 // Wave packing of the levelizer (backend.cpp); process-wide, default on
 // (env CVM_PACK=0 turns it off).
@@ -146,6 +130,7 @@ struct Node {
   int64_t slot;         // -1: pure constant
   int32_t sign;
   uint32_t constant;
+  uint32_t plan;        // 1-based index of the captured plan producing it, 0 = none
 };
 
 class GpuBackend final : public Backend {
@@ -170,7 +155,7 @@ class GpuBackend final : public Backend {
   // backend will not be used again).  Returns whether they were released.
   bool release_slots();
   void flush();                             // everything pending
-  void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only
+  void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only (validated)
   // Flush policy of decrypt/export: the requested cone only (default) or
   // everything pending (for callers that decrypt bit by bit, like the
   // reference's decrypt_word loop, word.cpp:70-77).
@@ -190,6 +175,9 @@ class GpuBackend final : public Backend {
   std::vector<std::vector<cvm_gate>> pack_levels(std::vector<Bit> ids, uint32_t depth) const;
   void run(const std::vector<Bit>& ids);
   void retire(const std::vector<Bit>& done);
+  void flush_locked();
+  void flush_for_locked(size_t n, const Bit* hs);
+  void check_captured(const Node& n) const;
 
   std::mutex mu_;
   Context* ctx_;
@@ -209,6 +197,7 @@ class GpuBackend final : public Backend {
   std::vector<std::string> regions_;
   uint64_t fences_ = 0;
   cvm_backend_stats stats_{};
+  std::vector<std::shared_ptr<std::atomic<bool>>> plans_;  // captured plans: ran yet?
 };
 
 // Cleartext recorder: the SimBackend semantics (sim_backend.cpp:25-154) with
@@ -240,44 +229,13 @@ class ClearBackend final : public Backend {
   cvm_backend_stats stats_{};
 };
 
-// ------------------------------------------------------ functional units --
-namespace alu {
-struct AddResult {
-  Word sum;
-  Bit carry_out;
-};
-struct Flags {
-  Bit n, z, c, v;
-};
-enum class ShiftKind { LogicalLeft, LogicalRight, ArithmeticRight };
-enum class BitwiseKind { And, Or, Xor, OrNot };
-enum class DivAccumulator { Widened, Exact };
-
-AddResult add(Backend& bk, const Word& a, const Word& b);
-AddResult add(Backend& bk, const Word& a, const Word& b, Bit carry_in);
-AddResult sub(Backend& bk, const Word& a, const Word& b);
-AddResult add_sub_select(Backend& bk, const Word& a, const Word& b, Bit subtract);
-Word shift_imm(Backend& bk, const Word& w, ShiftKind kind, unsigned amount);
-Word shift_reg(Backend& bk, const Word& w, ShiftKind kind, const Word& amount);
-Word mul_unsigned(Backend& bk, const Word& a, const Word& b);
-Word mul_signed(Backend& bk, const Word& a, const Word& b);
-Word div_unsigned(Backend& bk, const Word& n, const Word& d,
-                  DivAccumulator mode = DivAccumulator::Widened);
-Word bitwise(Backend& bk, BitwiseKind kind, const Word& a, const Word& b);
-Word not_word(Backend& bk, const Word& a);
-Word constant_word(Backend& bk, uint64_t value, unsigned width);
-Bit or_reduce(Backend& bk, const Word& w);
-Flags flags(Backend& bk, const Word& result, Bit carry_out, Bit a_msb, Bit b_msb);
-}  // namespace alu
-
-// Applies one cvm_fu_op; returns the output bits.
-Word fu_apply(Backend& bk, uint32_t op, const Word& a, const Word& b, Bit c);
-int fu_out_width(uint32_t op, uint32_t width);
-
-// Straight-line emulator (Machine, emulator.cpp:134-369).
-void machine_run(Backend& bk, unsigned word_size, unsigned register_count,
-                 const std::vector<Word>& memory, const cvm_insn* program,
-                 uint32_t count, std::vector<Word>* regs, alu::Flags* nzcv);
+// ---------------------------------------------------------- circuit replay --
+// A recorded circuit (cvm_dag_node table, the reference GateDag's node shape)
+// re-issued as Backend calls; handles[i] receives node i+1's handle.  Inputs
+// are consumed in node order by the table's input nodes (dag.cpp).
+void validate_dag(const cvm_dag_node* nodes, uint64_t n, uint64_t* n_inputs);
+void replay_dag(Backend& bk, const cvm_dag_node* nodes, uint64_t n, const Bit* inputs,
+                uint64_t n_inputs, Bit* handles);
 
 }  // namespace cvm
 

@@ -580,7 +580,7 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
       break;
     case 7: {
       if (!kskb) return cudaErrorInvalidValue;
-      static bool configured = false;
+      static std::atomic<uint64_t> configured{0};
       const int smem = int(sizeof(KsmSmem));
       cudaError_t e = set_smem(key_switch_mma_kernel, smem, configured);
       if (e != cudaSuccess) return e;
@@ -590,7 +590,7 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
     }
     case 8: {
       if (!ksktc) return cudaErrorInvalidValue;
-      static bool configured = false;
+      static std::atomic<uint64_t> configured{0};
       const int smem = int(sizeof(KsTcSmem));
       cudaError_t e = set_smem(key_switch_tc_kernel, smem, configured);
       if (e != cudaSuccess) return e;
@@ -601,7 +601,7 @@ cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe
     }
     case 9: {  // split-K tcgen05 product: ~148 CTAs whatever the level width
       if (!ksktc || !kspart) return cudaErrorInvalidValue;
-      static bool configured = false;
+      static std::atomic<uint64_t> configured{0};
       const int smem = int(sizeof(KsTcSmem));
       cudaError_t e = set_smem(key_switch_tc_kernel, smem, configured);
       if (e != cudaSuccess) return e;

@@ -3,6 +3,7 @@
 // cp.async, tcgen05 / tensor-memory helpers, and the launch-time dynamic
 // shared-memory opt-in.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -135,10 +136,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 // Opt a kernel into more than 48 KB of dynamic shared memory, once.
 template <class K>
-inline cudaError_t set_smem(K* kern, int bytes, bool& configured) {
-  if (configured) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) configured = true;
+// The dynamic shared-memory opt-in is per device: `configured` holds one bit
+// per device ordinal (ordinals >= 64 set the attribute on every launch).
+inline cudaError_t set_smem(K* kern, int bytes, std::atomic<uint64_t>& configured) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (bit && (configured.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) configured.fetch_or(bit, std::memory_order_release);
   return e;
 }
 

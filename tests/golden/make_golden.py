@@ -51,6 +51,12 @@ def parse_dag(lines):
     return np.array(nodes, dtype=np.int64), np.array(outs, dtype=np.int64)
 
 
+FIXED = [("umul", 16, 0xFFFF, 0xFFFF), ("smul", 16, 0xFFFF, 0xFFFF), ("smul", 16, 0x8000, 2),
+         ("udiv", 8, 0, 0), ("udiv", 8, 1, 0), ("udiv", 8, 77, 0), ("udiv", 8, 255, 0),
+         ("udiv", 16, 12345, 0), ("udiv", 16, 0xFFFF, 0),
+         ("udiv_exact", 4, 13, 7), ("udiv", 4, 13, 7)]
+
+
 def main():
     if not os.path.exists(DRIVER):
         sys.exit("build the reference driver first: make -C oracle ref")
@@ -74,7 +80,15 @@ def main():
                 rows.append([int(f[3]), int(f[4]), int(f[5]), f[6]])
         vectors[op] = rows
     # Fixed examples the reference tests single out
-    # (alu_shift_mul_div_test.cc: 0xFFFF*0xFFFF, divisor 0).
+    # (proj/tests/alu_shift_mul_div_test.cc): MaxOperands 0xFFFF * 0xFFFF
+    # (:198-203), SignHandling -1 * -1 and INT_MIN * 2 (:228-237),
+    # DivisorZeroGivesAllOnes (:316-325, plus the 16-bit case),
+    # ExactModeOverflowsOnLargeDivisors 13 / 7 (:341-349, both modes).
+    fixed = []
+    for op, w, a, b in FIXED:
+        f = run("one", op, w, a, b, 0)[0].split()
+        fixed.append([op, w, int(f[3]), int(f[4]), int(f[5]), f[6]])
+    vectors["fixed"] = fixed
     with gzip.open(os.path.join(HERE, "vectors.json.gz"), "wt") as fh:
         json.dump(vectors, fh)
 

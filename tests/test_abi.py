@@ -37,7 +37,24 @@ def test_struct_layouts():
     # cvm_gate: kind, pad, 3 x cvm_operand(16 B), out_slot
     assert ctypes.sizeof(N.Operand) == 16
     assert ctypes.sizeof(N.Gate) == 8 + 48 + 8
-    assert ctypes.sizeof(N.Insn) == 40
+    # cvm_dag_node: kind, input, value, ndeps, pad, dep[3]
+    assert ctypes.sizeof(N.DagNode) == 32 == P.DAG_DTYPE.itemsize
+
+
+def test_dag_batch_checks_buffer_sizes_before_touching_them():
+    """cvm_dag_batch validates the table and the element counts of both host
+    buffers against it (no over-read on mismatched shapes).  A
+    NULL context is rejected first, so this runs without a GPU."""
+    import numpy as np
+    st = N.BackendStats()
+    nodes = np.zeros(3, P.DAG_DTYPE)
+    nodes["input"][:2] = 1
+    nodes["kind"][2], nodes["ndeps"][2] = P.KIND["AND"], 2
+    nodes["dep"][2, :2] = (1, 2)
+    outs = np.array([3], np.uint64)
+    with pytest.raises(P.CvmInputError):
+        N.check(N.lib.cvm_dag_batch(None, nodes.ctypes.data, 3, outs.ctypes.data, 1, 1,
+                                    None, 0, None, 0, ctypes.byref(st)))
 
 
 def test_version_and_errors():

@@ -1,85 +1,130 @@
-"""Host logic against the reference's golden fixtures (no GPU needed).
+"""Recorded circuits against the reference's golden fixtures (no GPU needed).
 
-tests/golden/ was produced by running the reference implementation itself
-(oracle/ref_golden.cpp linked against /root/reference/proj/core/src, script
-tests/golden/make_golden.py).  These tests check that the product's C++
-functional units and machine (paper_2101_03403_b200/csrc/alu.cpp,
-machine.cpp), recorded through the cleartext recorder, emit exactly the
-reference's gate DAG node for node and compute the reference's results.
+The B200 library holds no copy of the reference's functional units or
+emulator: the reference records them (integration/cryptovm_dag_export.cpp,
+driving the unmodified alu.cpp / emulator.cpp compiled from /root/reference)
+and the library replays the table (cvm_backend_replay_dag / cvm_dag_batch).
+These tests check, on the cleartext recorder (SimBackend semantics):
+  * the live recorder (integration/refshim.py) emits exactly the golden DAGs
+    that tests/golden/make_golden.py stored from the reference run;
+  * replaying a table re-creates it node for node;
+  * replayed circuits compute the reference's golden results, including the
+    fixed examples the reference's own tests single out.
 """
 import gzip
 import json
 import os
+import sys
 
 import numpy as np
 import pytest
 
 import paper_2101_03403_b200 as P
+from conftest import GOLD, USES_C, fu_dag, program_dag
 
-GOLD = os.path.join(os.path.dirname(__file__), "golden")
+sys.path.insert(0, os.path.join(os.path.dirname(GOLD), "..", "integration"))
+import refshim  # noqa: E402
+
 DAGS = np.load(os.path.join(GOLD, "dags.npz"))
 with gzip.open(os.path.join(GOLD, "vectors.json.gz"), "rt") as fh:
     VECTORS = json.load(fh)
 PROGRAMS = json.load(open(os.path.join(GOLD, "programs.json")))
-PROG_ARR = np.load(os.path.join(GOLD, "programs.npz"))
-
-USES_C = {"add_cin", "addsub"}
-# ops with a reference fixture; "mul_lo" (the emulator's MUL) is checked below
-REF_OPS = [op for op in P.FU_OPS if op != "mul_lo"]
+REF_OPS = [op for op in refshim.FU_OPS if op != "mul_lo"]
+need_shim = pytest.mark.skipif(not refshim.available(),
+                               reason="libcvm_refshim.so not built (needs /root/reference)")
 
 
-def _record(op, w, av=0, bv=0, cv=0):
-    b = P.Backend()  # cleartext recorder
-    a = b.encrypt_word(av, w)
-    bb = b.encrypt_word(bv, w)
-    c = b.encrypt_bit(cv) if op in USES_C else 0
-    return b, b.fu(op, a, bb, c)
+def _replay_clear(dag, in_bits):
+    """Replay on the cleartext recorder: returns (backend, output handles)."""
+    b = P.Backend()
+    ins = np.array([b.encrypt_bit(int(x)) for x in in_bits], np.uint64)
+    return b, b.replay_outputs(dag, ins)
 
 
+def _operand_bits(op, w, av, bv, cv):
+    bits = [(av >> i) & 1 for i in range(w)] + [(bv >> i) & 1 for i in range(w)]
+    return bits + ([cv] if op in USES_C else [])
+
+
+@need_shim
 @pytest.mark.parametrize("w", [4, 8, 16])
 @pytest.mark.parametrize("op", REF_OPS)
-def test_dag_identical_to_reference(op, w):
-    b, out = _record(op, w)
-    gold = DAGS[f"{op}_{w}_nodes"]
-    mine = b.nodes()
-    assert mine.shape == gold.shape
-    assert np.array_equal(mine, gold)
-    assert np.array_equal(out, DAGS[f"{op}_{w}_out"])
+def test_recorder_emits_the_golden_dag(op, w):
+    d = refshim.record_fu(op, w)
+    assert np.array_equal(d.rows(), DAGS[f"{op}_{w}_nodes"])
+    assert np.array_equal(d.outputs, DAGS[f"{op}_{w}_out"])
+
+
+@need_shim
+@pytest.mark.parametrize("w", [4, 8, 16])
+def test_recorder_mul_lo_is_umul_low_half(w):
+    """MUL as Machine::execute issues it (emulator.cpp:271-285): the
+    mul_unsigned DAG, low half kept."""
+    d = refshim.record_fu("mul_lo", w)
+    assert np.array_equal(d.rows(), DAGS[f"umul_{w}_nodes"])
+    assert np.array_equal(d.outputs, DAGS[f"umul_{w}_out"][:w])
+
+
+@need_shim
+@pytest.mark.parametrize("idx", range(len(PROGRAMS)))
+def test_recorder_program_dag_is_golden(idx):
+    dag, meta = program_dag(idx)
+    rec = refshim.record_program([tuple(i) for i in meta["insns"]], len(meta["mem"]))
+    assert np.array_equal(rec.rows(), dag.rows())
+    assert np.array_equal(rec.outputs, dag.outputs)
+
+
+@pytest.mark.parametrize("w", [4, 16])
+@pytest.mark.parametrize("op", ["add", "cmp", "lsl", "umul", "udiv", "addsub"])
+def test_replay_recreates_the_table(op, w):
+    dag = fu_dag(op, w)
+    b, _ = _replay_clear(dag, np.zeros(dag.n_inputs, np.uint8))
+    assert np.array_equal(b.nodes(), dag.rows())
 
 
 @pytest.mark.parametrize("op", REF_OPS)
 def test_vectors_match_reference(op):
-    # the operand width is implied by the result length (distinct per width)
-    width_of = {P.api.lib.cvm_fu_out_width(P.FU[op], wd): wd for wd in (4, 8, 16)}
+    """Every golden vector (exhaustive at width 4, seeded at 8 and 16)."""
+    dags = {}
     for av, bv, cv, bits in VECTORS[op]:
-        w = width_of[len(bits)]
-        b, out = _record(op, w, av, bv, cv)
-        got = "".join(str(x) for x in b.decrypt_bits(out))
-        assert got == bits, (op, w, av, bv, cv)
+        w = next(wd for wd in (4, 8, 16) if len(fu_dag(op, wd).outputs) == len(bits))
+        dag = dags.setdefault(w, fu_dag(op, w))
+        b, out = _replay_clear(dag, _operand_bits(op, w, av, bv, cv))
+        assert "".join(str(x) for x in b.decrypt_bits(out)) == bits, (op, w, av, bv, cv)
 
 
-def test_reference_edge_examples():
-    """Fixed examples the reference tests single out
-    (alu_shift_mul_div_test.cc): 0xFFFF * 0xFFFF and division by zero."""
-    b, out = _record("umul", 16, 0xFFFF, 0xFFFF)
-    assert b.decrypt_word(out) == 0xFFFE0001
-    b, out = _record("udiv", 8, 200, 0)
-    assert b.decrypt_word(out) == 0xFF
-    b, out = _record("udiv_exact", 4, 13, 7)  # exact-mode overflow case
-    want = [v for v in VECTORS["udiv_exact"] if v[0] == 13 and v[1] == 7][0][3]
-    assert "".join(str(x) for x in b.decrypt_bits(out)) == want
+def test_reference_fixed_examples():
+    """The fixed examples of the reference's own tests, as the reference run
+    recorded them (vectors["fixed"], tests/golden/make_golden.py FIXED):
+    0xFFFF x 0xFFFF = 0xFFFE0001 (alu_shift_mul_div_test.cc:198-203), signed
+    -1 x -1 and INT_MIN x 2 (:228-237), divisor 0 -> all ones (:316-325),
+    13 / 7 exact-mode overflow vs widened (:341-349)."""
+    fixed = VECTORS["fixed"]
+    assert len(fixed) == 11
+    expect = {("umul", 16, 0xFFFF, 0xFFFF): 0xFFFE0001, ("smul", 16, 0xFFFF, 0xFFFF): 1,
+              ("smul", 16, 0x8000, 2): 0xFFFF0000, ("udiv", 4, 13, 7): 1}
+    for op, w, av, bv, cv, bits in fixed:
+        b, out = _replay_clear(fu_dag(op, w), _operand_bits(op, w, av, bv, cv))
+        assert "".join(str(x) for x in b.decrypt_bits(out)) == bits, (op, w, av, bv)
+        val = int(bits[::-1], 2)
+        if (op, w, av, bv) in expect:
+            assert val == expect[(op, w, av, bv)]
+        elif op == "udiv":
+            assert val == (1 << w) - 1  # divisor 0
+        else:
+            assert op == "udiv_exact" and val != 1  # the documented overflow
 
 
-@pytest.mark.parametrize("meta", PROGRAMS, ids=[f"seed{m['seed']}" for m in PROGRAMS])
-def test_config5_program_matches_reference(meta):
-    b = P.Backend()
-    mem = [b.encrypt_word(v, 16) for v in meta["mem"]]
-    prog = [tuple(i) for i in meta["insns"]]
-    regs, nzcv = b.machine_run(prog, mem)
-    assert [b.decrypt_word(r) for r in regs] == meta["regs"]
-    assert list(b.decrypt_bits(nzcv)) == meta["nzcv"]
-    gold = PROG_ARR[f"p{meta['seed']}_nodes"]
-    assert np.array_equal(b.nodes(), gold)
+@pytest.mark.parametrize("idx", range(len(PROGRAMS)))
+def test_config5_program_replay_matches_reference(idx):
+    dag, meta = program_dag(idx)
+    bits = [(v >> i) & 1 for v in meta["mem"] for i in range(16)]
+    b, out = _replay_clear(dag, bits)
+    vals = b.decrypt_bits(out)
+    regs = [int((vals[16 * r:16 * r + 16].astype(np.int64) << np.arange(16)).sum())
+            for r in range(8)]
+    assert regs == meta["regs"]
+    assert list(vals[128:]) == meta["nzcv"]
 
 
 def test_level_statistics_match_survey():
@@ -87,9 +132,10 @@ def test_level_statistics_match_survey():
     expect = {("add", 16): (195, 9), ("cmp", 16): (217, 14), ("lsl", 16): (64, 4),
               ("umul", 16): (3376, 118), ("udiv", 16): (4016, 208), ("and", 16): (16, 1)}
     for (op, w), (gates, levels) in expect.items():
-        b, _ = _record(op, w)
+        dag = fu_dag(op, w)
+        b, _ = _replay_clear(dag, np.zeros(dag.n_inputs, np.uint8))
         st = b.stats()
-        assert st["bootstrapped"] == gates, op
+        assert st["bootstrapped"] == gates == dag.bootstrapped(), op
         assert st["levels_run"] == levels, op
 
 
@@ -104,21 +150,24 @@ def test_input_errors_mirror_reference():
         b.unary_gate("AND", h)  # not a unary gate (sim_backend.cpp:80-83)
     with pytest.raises(P.CvmInputError):
         b.pop_region()  # unbalanced (sim_backend.cpp:140-142)
-    with pytest.raises(P.CvmInputError):
-        b.fu("add", np.array([h, h], np.uint64), np.array([h], np.uint64))  # width mismatch
-    with pytest.raises(P.CvmInputError):
-        b.fu("lsl", np.array([h] * 3, np.uint64), np.array([h] * 3, np.uint64))  # not 2^k
 
 
-@pytest.mark.parametrize("w", [4, 8, 16])
-def test_mul_lo_is_the_reference_umul_dag_low_half(w):
-    """mul_lo records exactly the reference mul_unsigned DAG and returns its
-    low half -- what Machine::execute keeps for MUL (emulator.cpp:271-285)."""
-    b, out = _record("mul_lo", w)
-    assert np.array_equal(b.nodes(), DAGS[f"umul_{w}_nodes"])
-    assert np.array_equal(out, DAGS[f"umul_{w}_out"][:w])
-    for av, bv, cv, bits in VECTORS["umul"]:
-        if len(bits) != 2 * w:
-            continue
-        b, out = _record("mul_lo", w, av, bv)
-        assert "".join(str(x) for x in b.decrypt_bits(out)) == bits[:w]
+def test_replay_rejects_malformed_tables():
+    dag = fu_dag("add", 4)
+    b = P.Backend()
+    ins = np.array([b.encrypt_bit(0) for _ in range(dag.n_inputs)], np.uint64)
+    with pytest.raises(P.CvmInputError):
+        b.replay(dag, ins[:-1])  # input count differs from the table's
+    bad = P.Dag(dag.nodes.copy(), dag.outputs)
+    i = int(np.flatnonzero(bad.nodes["kind"] == P.KIND["AND"])[0])
+    bad.nodes["dep"][i, 0] = i + 1  # refers to itself: not an earlier node
+    with pytest.raises(P.CvmInputError):
+        b.replay(bad, ins)
+    bad = P.Dag(dag.nodes.copy(), dag.outputs)
+    bad.nodes["ndeps"][i] = 3  # a binary gate with three operands
+    with pytest.raises(P.CvmInputError):
+        b.replay(bad, ins)
+    bad = P.Dag(dag.nodes.copy(), dag.outputs)
+    bad.nodes["kind"][i] = 14  # no such GateKind
+    with pytest.raises(P.CvmInputError):
+        b.replay(bad, ins)

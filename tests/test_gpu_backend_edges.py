@@ -1,13 +1,14 @@
 """Backend contract edge cases on the device path (gates.hpp:109-132 semantics,
 SURVEY §8 a-2, a-5, a-7, a-16): folded free ops at export time, blob round
 trips and the InputError paths, plan replay on new inputs, slab growth,
-scratch-slot reuse by cvm_fu_batch, and concurrent recording."""
+scratch-slot reuse by cvm_dag_batch, and concurrent recording."""
 import threading
 
 import numpy as np
 import pytest
 
 import paper_2101_03403_b200 as P
+from conftest import fu, fu_batch
 from paper_2101_03403_b200._native import CvmInputError, lib
 
 pytestmark = pytest.mark.gpu
@@ -59,7 +60,7 @@ def test_plan_replay_on_new_inputs(keyset, ctx):
     bk = P.Backend(ctx, keyset)
     a = bk.import_lwe(keyset.encrypt_words(np.array([0]), 8, 1).reshape(-1, 631))
     b = bk.import_lwe(keyset.encrypt_words(np.array([0]), 8, 2).reshape(-1, 631))
-    outs = bk.fu("add", a, b)
+    outs = fu(bk, "add", a, b)
     plan = bk.capture_plan()
     assert plan.info()["gates"] > 0
     slots_a = [bk.handle_slot(h)[0] for h in a]
@@ -99,10 +100,10 @@ def test_slab_growth_preserves_contents(keyset, ctx):
 def test_fu_batch_reuses_its_scratch_slots(keyset, ctx):
     a = keyset.encrypt_words(np.arange(32) * 7 % 65536, 16, 3)
     b = keyset.encrypt_words(np.arange(32) * 13 % 65536, 16, 4)
-    P.fu_batch(ctx, "add", 16, a, b)
+    fu_batch(ctx, "add", 16, a, b)
     used = lib.cvm_slots_capacity(ctx.handle)
     for _ in range(3):
-        out, st = P.fu_batch(ctx, "add", 16, a, b)
+        out, st = fu_batch(ctx, "add", 16, a, b)
     assert lib.cvm_slots_capacity(ctx.handle) == used
     sums = keyset.decrypt_words(out.reshape(-1, 631), 17)
     assert np.array_equal(sums, (np.arange(32) * 7 % 65536) + (np.arange(32) * 13 % 65536))

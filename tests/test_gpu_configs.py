@@ -1,35 +1,44 @@
 """Configs 2-5 on the GPU: decrypted results equal the reference SimBackend's
-golden results (tests/golden/, produced by running the reference itself)."""
+golden results (tests/golden/, produced by running the reference itself),
+for circuits the reference recorded (replayed by cvm_dag_batch)."""
 import gzip
 import json
 import os
+import sys
 
 import numpy as np
 import pytest
 
 import paper_2101_03403_b200 as P
+from conftest import GOLD, USES_C, fu, fu_batch, fu_dag, program_dag
+
+sys.path.insert(0, os.path.join(os.path.dirname(GOLD), "..", "integration"))
+import refshim  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-GOLD = os.path.join(os.path.dirname(__file__), "golden")
 with gzip.open(os.path.join(GOLD, "vectors.json.gz"), "rt") as fh:
     VECTORS = json.load(fh)
 PROGRAMS = json.load(open(os.path.join(GOLD, "programs.json")))
+ALL_OPS = ["add", "add_cin", "sub", "addsub", "cmp", "and", "orr", "eor", "orn", "lsl",
+           "lsr", "asr", "umul", "smul", "udiv", "udiv_exact"]
+need_shim = pytest.mark.skipif(not refshim.available(),
+                               reason="libcvm_refshim.so not built (needs /root/reference)")
 
 
-def _golden(op, width, limit):
-    ow = P.api.lib.cvm_fu_out_width(P.FU[op], width)
+def _golden(op, width, limit=None):
+    ow = len(fu_dag(op, width).outputs)
     rows = [r for r in VECTORS[op] if len(r[3]) == ow]
-    return rows[:limit]
+    return rows[:limit] if limit else rows
 
 
 def _run_batch(keyset, ctx, op, width, rows, seed):
     a = keyset.encrypt_words([r[0] for r in rows], width, seed)
     b = keyset.encrypt_words([r[1] for r in rows], width, seed + 1)
     c = None
-    if op in ("add_cin", "addsub"):
+    if op in USES_C:
         c = keyset.encrypt(np.array([r[2] for r in rows], np.uint8), seed + 2)
-    out, st = P.fu_batch(ctx, op, width, a, b, c)
+    out, st = fu_batch(ctx, op, width, a, b, c)
     bits = keyset.decrypt(out.reshape(-1, 631)).reshape(len(rows), -1)
     return ["".join(str(x) for x in row) for row in bits], st
 
@@ -39,9 +48,33 @@ def _run_batch(keyset, ctx, op, width, rows, seed):
                                   ("orn", 16), ("lsl", 16), ("lsr", 16), ("asr", 8)])
 def test_config2_3_units_16bit(op, n, keyset, ctx):
     rows = _golden(op, 16, n)
-    got, st = _run_batch(keyset, ctx, op, 16, rows, 300 + P.FU[op] * 7)
+    got, st = _run_batch(keyset, ctx, op, 16, rows, 300 + ALL_OPS.index(op) * 7)
     assert got == [r[3] for r in rows]
     assert st["bootstrapped"] > 0
+
+
+@pytest.mark.parametrize("op", ALL_OPS)
+def test_exhaustive_width4_every_op(op, keyset, ctx):
+    """Every operand combination at width 4 (the reference's exhaustive
+    vectors, incl. the carry / select input) in one batch through CUDA."""
+    rows = _golden(op, 4)
+    assert len(rows) == 256 * (2 if op in USES_C else 1)
+    got, _ = _run_batch(keyset, ctx, op, 4, rows, 1000 + ALL_OPS.index(op) * 7)
+    assert got == [r[3] for r in rows]
+
+
+def test_reference_fixed_examples_on_gpu(keyset, ctx):
+    """The reference tests' fixed examples through CUDA, against the outputs
+    the reference run recorded (vectors["fixed"]): 0xFFFF x 0xFFFF =
+    0xFFFE0001 (alu_shift_mul_div_test.cc:198-203), signed -1 x -1 = 1 and
+    INT_MIN x 2 (:228-237), divisor 0 -> all ones at 8 and 16 bits
+    (:316-325), 13 / 7 in exact and widened mode (:341-349)."""
+    for k, (op, w, av, bv, cv, bits) in enumerate(VECTORS["fixed"]):
+        a = keyset.encrypt_words([av], w, 1500 + 2 * k)
+        b = keyset.encrypt_words([bv], w, 1501 + 2 * k)
+        out, _ = fu_batch(ctx, op, w, a, b)
+        got = "".join(str(x) for x in keyset.decrypt(out.reshape(-1, 631)))
+        assert got == bits, (op, w, av, bv)
 
 
 def test_config4_mul16(keyset, ctx):
@@ -51,39 +84,17 @@ def test_config4_mul16(keyset, ctx):
     assert st["last_flush_levels"] == 118
 
 
-def test_div16_and_smul16(keyset, ctx):
-    for op, seed in (("udiv", 601), ("smul", 611)):
-        rows = _golden(op, 16, 4)
-        got, _ = _run_batch(keyset, ctx, op, 16, rows, seed)
-        assert got == [r[3] for r in rows], op
-
-
-def test_config5_program_on_gpu(keyset, ctx):
-    """BASELINE configs[4]: 8 encrypted 16-bit registers, 64 random
-    instructions + UDIV, dataflow-scheduled across instruction fences."""
-    meta = PROGRAMS[0]
-    bk = P.Backend(ctx, keyset)
-    mem_ct = keyset.encrypt_words(meta["mem"], 16, 701)
-    mem = [bk.import_lwe(w) for w in mem_ct]
-    regs, nzcv = bk.machine_run([tuple(i) for i in meta["insns"]], mem)
-    # the key owner decrypts the final state: one flush, evaluating only the
-    # cone of influence of the 8 registers and NZCV (dead gates skipped)
-    bits = bk.decrypt_bits(np.concatenate([regs.ravel(), nzcv]))
-    words = bits[:128].reshape(8, 16).astype(np.int64)
-    vals = [int((w << np.arange(16)).sum()) for w in words]
-    assert vals == meta["regs"]
-    assert list(bits[128:]) == meta["nzcv"]
-    st = bk.stats()
-    assert st["flushes"] == 1  # one flush for the whole program (no branches)
-    assert st["bootstrapped"] == 26038  # recorded, as the reference DAG
-    assert st["executed"] == 8483       # live cone of the outputs in that DAG
-    assert st["pending"] == 26038 - 8483
+@pytest.mark.parametrize("op", ["udiv", "smul", "udiv_exact"])
+def test_div16_and_smul16(op, keyset, ctx):
+    rows = _golden(op, 16, 16)
+    got, _ = _run_batch(keyset, ctx, op, 16, rows, 601 + ALL_OPS.index(op))
+    assert got == [r[3] for r in rows], op
 
 
 def _live_gates(nodes, outs):
     """Bootstrapped gates in the cone of influence of `outs` (reference DAG)."""
     mark = np.zeros(len(nodes), bool)
-    stack = list(outs)
+    stack = list(int(o) for o in outs)
     while stack:
         i = stack.pop()
         if mark[i - 1]:
@@ -95,19 +106,79 @@ def _live_gates(nodes, outs):
     return int((boot & mark).sum())
 
 
+@pytest.mark.parametrize("idx", range(len(PROGRAMS)))
+def test_config5_programs_on_gpu(idx, keyset, ctx):
+    """BASELINE configs[4], all three golden programs: 8 encrypted 16-bit
+    registers, 64 random instructions + UDIV, the reference Machine's recorded
+    DAG replayed with dataflow scheduling across the instruction fences; only
+    the live cone of the final registers and NZCV runs."""
+    dag, meta = program_dag(idx)
+    mem = keyset.encrypt_words(meta["mem"], 16, 701 + idx)
+    out, st = P.dag_batch(ctx, dag, mem.reshape(1, -1, 631))
+    bits = keyset.decrypt(out.reshape(-1, 631))
+    words = bits[:128].reshape(8, 16).astype(np.int64)
+    assert [int((w << np.arange(16)).sum()) for w in words] == meta["regs"]
+    assert list(bits[128:]) == meta["nzcv"]
+    assert st["flushes"] == 1
+    assert st["executed"] == _live_gates(dag.rows(), dag.outputs)
+    if idx == 0:
+        assert st["bootstrapped"] == 26038 and st["executed"] == 8483
+
+
+@need_shim
+def test_config5_reference_machine_through_the_shim(keyset, ctx):
+    """The reference's own Machine on cryptovm::GpuBackend (the drop-in):
+    demand-driven, so the live 8,483 of 26,038 recorded gates run."""
+    meta = PROGRAMS[0]
+    regs, nzcv, st, _ = refshim.run_program_gpu(ctx, keyset, [tuple(i) for i in meta["insns"]],
+                                                meta["mem"])
+    assert [int(r) for r in regs] == meta["regs"]
+    assert list(nzcv) == meta["nzcv"]
+    assert st["bootstrapped"] == 26038
+    assert st["executed"] == 8483
+
+
+@need_shim
+def test_reference_branchy_program_through_the_shim(keyset, ctx):
+    """Branches resolve through the reference's LocalBranchOracle (a
+    decrypt_bit of the flags, i.e. a demand-driven flush): 13 x 11 by a loop
+    (emulator_test.cc-style), 11 branch queries."""
+    prog = [dict(op="MOV", rd=0, has_imm=1, imm=0), dict(op="MOV", rd=1, has_imm=1, imm=13),
+            dict(op="MOV", rd=2, has_imm=1, imm=11),
+            dict(op="ADD", rd=0, rn=0, rm=1),
+            dict(op="SUBS", rd=2, rn=2, has_imm=1, imm=1, sets_flags=1),
+            dict(op="B", cond="NE", has_target=1, target=3), dict(op="HALT")]
+    for x in prog:
+        x.setdefault("rn", -1)
+        x.setdefault("rm", -1)
+        x.setdefault("rd", -1)
+    regs, _, st, bq = refshim.run_program_gpu(ctx, keyset, prog, [], max_steps=1000)
+    assert int(regs[0]) == 143 and int(regs[2]) == 0
+    assert bq == 11
+
+
+@need_shim
+def test_reference_add_api_through_the_shim(keyset, ctx):
+    rng = np.random.default_rng(9)
+    a, b = rng.integers(0, 1 << 16, 24), rng.integers(0, 1 << 16, 24)
+    sums, carries, st = refshim.add_batch_gpu(ctx, keyset, a, b, 16)
+    assert np.array_equal(sums + (carries.astype(np.uint64) << 16), a + b)
+    assert st["flushes"] == 1
+
+
 def test_demand_driven_flush_keeps_dead_gates_pending(keyset, ctx):
     """Decrypting the low half of a MUL16 evaluates exactly the cone of those
     16 bits in the reference DAG (1,293 of 3,376 gates); asking for the high
     half afterwards evaluates the remaining live gates, same results."""
-    d = np.load(os.path.join(GOLD, "dags.npz"))
-    nodes, outs = d["umul_16_nodes"], d["umul_16_out"]
+    dag = fu_dag("umul", 16)
+    nodes, outs = dag.rows(), dag.outputs
     lo_live = _live_gates(nodes, outs[:16])
     all_live = _live_gates(nodes, outs)
     assert lo_live == 1293
     bk = P.Backend(ctx, keyset)
     a = bk.import_lwe(keyset.encrypt_words([0xBEEF], 16, 801)[0])
     b = bk.import_lwe(keyset.encrypt_words([0x1234], 16, 802)[0])
-    p = bk.fu("umul", a, b)
+    p = fu(bk, "umul", a, b)
     assert bk.decrypt_word(p[:16]) == (0xBEEF * 0x1234) & 0xFFFF
     st = bk.stats()
     assert st["executed"] == lo_live and st["pending"] == 3376 - lo_live

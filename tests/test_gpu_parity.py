@@ -12,6 +12,7 @@ import pytest
 
 import oracle as O
 import paper_2101_03403_b200 as P
+from conftest import fu, fu_batch
 
 pytestmark = pytest.mark.gpu
 
@@ -150,7 +151,7 @@ def test_wave_packing_same_results(op, keyset, ctx):
     try:
         for pack in (1, 0):
             check(lib.cvm_set_level_packing(pack))
-            res[pack] = P.fu_batch(ctx, op, 16, a, b)
+            res[pack] = fu_batch(ctx, op, 16, a, b)
     finally:
         check(lib.cvm_set_level_packing(old))
     (o1, s1), (o0, s0) = res[1], res[0]
@@ -250,7 +251,7 @@ def test_add16_through_backend_matches_oracle_dag(keyset, ctx, oracle_keys):
     ref = O.eval_dag(oracle_keys, nodes, np.concatenate([ca, cb]))
     bk = P.Backend(ctx, keyset)
     ha, hb = bk.import_lwe(ca), bk.import_lwe(cb)
-    out = bk.fu("add", ha, hb)
+    out = fu(bk, "add", ha, hb)
     got = bk.export_lwe(out)
     assert np.array_equal(got, ref[outs - 1])
     assert bk.decrypt_word(out[:16]) == (av + bv) & 0xFFFF
@@ -264,7 +265,7 @@ def test_fu_batch_add16_decrypts(keyset, ctx):
     bv = rng.integers(0, 1 << 16, batch)
     a = keyset.encrypt_words(av, 16, 51)
     b = keyset.encrypt_words(bv, 16, 52)
-    out, st = P.fu_batch(ctx, "add", 16, a, b)
+    out, st = fu_batch(ctx, "add", 16, a, b)
     vals = keyset.decrypt_words(out.reshape(-1, 631), 17)
     assert np.array_equal(vals, (av + bv) % (1 << 17))
     assert st["last_flush_levels"] == 9

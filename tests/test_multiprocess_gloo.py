@@ -25,6 +25,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     import paper_2101_03403_b200 as P
+    from conftest import fu
     ws, r, local = bench.dist_env()
     av, bv = bench.workload_operands(r)
     # record a slice of this rank's shard on the cleartext recorder
@@ -32,7 +33,7 @@ def _worker(rank, world, port, q):
     ok = True
     for i in range(4):
         wa, wb = b.encrypt_word(int(av[i]), 16), b.encrypt_word(int(bv[i]), 16)
-        out = b.fu("add", wa, wb)
+        out = fu(b, "add", wa, wb)
         ok &= b.decrypt_word(out) == int(av[i] + bv[i])
     gates = torch.tensor([b.stats()["bootstrapped"]], dtype=torch.float64)
     dist.all_reduce(gates, op=dist.ReduceOp.SUM)

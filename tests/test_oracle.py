@@ -2,8 +2,10 @@
 
 The reference ships no TFHE code, so ciphertext-level
 parity cannot be pinned to reference outputs; these tests pin the oracle to
-exact arithmetic instead, and tests/test_oracle_golden.py pins its decrypted
-results to the reference SimBackend's golden vectors.
+exact arithmetic instead; tests/test_gpu_parity.py replays the reference's
+recorded DAGs on the oracle and decrypts them to the reference SimBackend's
+golden results, and test_keygen_byte_identical_to_product below pins the
+product keygen to the oracle's.
 """
 import numpy as np
 import pytest
@@ -131,3 +133,21 @@ def test_eval_dag_free_ops_after_same_level_gates(sk, ck_ntt):
     assert np.array_equal(ct[4], (np.uint32(0) - ct[2]).astype(np.uint32))
     assert np.array_equal(ct[6], ct[4])
     assert list(sk.decrypt(ct[2:])) == [1, 1, 0, 1, 0]
+
+
+@pytest.mark.parametrize("seed", [SEED, 7])
+def test_keygen_byte_identical_to_product(seed):
+    """The product keygen (csrc/keys.cpp) and the oracle keygen
+    (oracle/tfhe_oracle.c) are independent implementations of one spec
+    (DESIGN.md section 3); they must produce the same key bytes and the same
+    fresh encryptions, which bench.py's CPU legs rely on."""
+    import paper_2101_03403_b200 as P
+    prod = P.KeySet(seed)
+    mine = prod.export()
+    ref = O.SecretKeys(seed)
+    for name in ("lwe_key", "tlwe_key", "bk", "ksk"):
+        a, b = mine[name], getattr(ref, name)
+        assert a.dtype.itemsize == b.dtype.itemsize and a.tobytes() == b.tobytes(), name
+    bits = np.random.default_rng(seed).integers(0, 2, 257).astype(np.uint8)
+    for enc_seed in (1, 12345):
+        assert prod.encrypt(bits, enc_seed).tobytes() == ref.encrypt(bits, enc_seed).tobytes()

@@ -48,10 +48,14 @@ def main():
     batch = int(os.environ.get("ADD_BATCH", 256))
     av, bv = rng.integers(0, 1 << 16, batch), rng.integers(0, 1 << 16, batch)
     wa, wb = ks.encrypt_words(av, 16, 3), ks.encrypt_words(bv, 16, 4)
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "integration"))
+    import refshim
+    add16 = refshim.record_fu("add", 16)
     for rep in range(2):
         ctx.reset_stats()
         t = time.time()
-        out, st = P.fu_batch(ctx, "add", 16, wa, wb)
+        out, st = P.dag_batch(ctx, add16, np.concatenate([wa, wb], axis=1))
         wall = time.time() - t
     ks_ = ctx.kernel_stats()
     vals = ks.decrypt_words(out.reshape(-1, 631), 17)
