@@ -119,6 +119,71 @@ CVM_HD void dft16(c64 v[16]) {
   for (int k = 0; k < 16; ++k) v[k] = o[k];
 }
 
+// The same DFT16 with the twiddled second-stage radix-4 butterflies fused
+// into FMAs (144 FP64 instructions instead of 160).  Columns k1 = 1 and 3
+// factor cos(pi/8) out of their two twiddles (t = tan(pi/8)), so the
+// butterfly sums become c * (P + t Q) -- one FMA per component -- and the
+// final adds absorb c as FMAs; column k1 = 2 absorbs 1/sqrt2 the same way.
+// The inverse is the forward transform with real and imaginary parts swapped
+// on input and output (swap(z) = i conj(z), so swap o DFT o swap = IDFT):
+// register renaming, no instructions.  Rounding differs from dft16 by a few ulp
+// (tests/native/fft_emul.cpp checks products and the rounding margin).
+constexpr double kTan8 = 0.41421356237309503;  // tan(pi/8)
+template <bool kInverse>
+CVM_HD void dft16f(c64 v[16]) {
+  if (kInverse) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = {v[i].y, v[i].x};
+  }
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<false>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  // Y[n2][k1] in v[4 k1 + n2]; X[k1 + 4 k2] = output k2 of column k1
+  c64 o[16];
+  {  // k1 = 0: no twiddles
+    c64 a = v[0], b = v[1], c = v[2], d = v[3];
+    dft4<false>(a, b, c, d);
+    o[0] = a, o[4] = b, o[8] = c, o[12] = d;
+  }
+  {  // k1 = 1: twiddles w16, w8, w16^3
+    const c64 Y0 = v[4], Y1 = v[5], Y2 = v[6], Y3 = v[7];
+    const double px = Y2.x + Y2.y, py = Y2.y - Y2.x;  // w8 Y2 = r p
+    const c64 a0 = {fma(kRsqrt2, px, Y0.x), fma(kRsqrt2, py, Y0.y)};
+    const c64 a1 = {fma(-kRsqrt2, px, Y0.x), fma(-kRsqrt2, py, Y0.y)};
+    const double A = Y1.x + Y3.y, B = Y1.y + Y3.x, C = Y1.y - Y3.x, D = Y3.y - Y1.x;
+    const double P1 = fma(kTan8, B, A), P2 = fma(kTan8, D, C);
+    const double P3 = fma(kTan8, C, -D), P4 = fma(-kTan8, A, B);
+    o[1] = {fma(kCos8, P1, a0.x), fma(kCos8, P2, a0.y)};
+    o[9] = {fma(-kCos8, P1, a0.x), fma(-kCos8, P2, a0.y)};
+    o[5] = {fma(kCos8, P4, a1.x), fma(-kCos8, P3, a1.y)};
+    o[13] = {fma(-kCos8, P4, a1.x), fma(kCos8, P3, a1.y)};
+  }
+  {  // k1 = 2: twiddles w8, -i, w8^3
+    const c64 Y0 = v[8], Y1 = v[9], Y2 = v[10], Y3 = v[11];
+    const c64 a0 = {Y0.x + Y2.y, Y0.y - Y2.x}, a1 = {Y0.x - Y2.y, Y0.y + Y2.x};
+    const double E = Y1.x + Y1.y, F = Y1.y - Y1.x, G = Y3.y - Y3.x, H = Y3.y + Y3.x;
+    const double b0x = E + G, b0y = F - H, dx = E - G, dy = F + H;  // b0, d / r
+    o[2] = {fma(kRsqrt2, b0x, a0.x), fma(kRsqrt2, b0y, a0.y)};
+    o[10] = {fma(-kRsqrt2, b0x, a0.x), fma(-kRsqrt2, b0y, a0.y)};
+    o[6] = {fma(kRsqrt2, dy, a1.x), fma(-kRsqrt2, dx, a1.y)};
+    o[14] = {fma(-kRsqrt2, dy, a1.x), fma(kRsqrt2, dx, a1.y)};
+  }
+  {  // k1 = 3: twiddles w16^3, w8^3, w16^9
+    const c64 Y0 = v[12], Y1 = v[13], Y2 = v[14], Y3 = v[15];
+    const double px = Y2.y - Y2.x, q = Y2.x + Y2.y;  // w8^3 Y2 = r (px, -q)
+    const c64 a0 = {fma(kRsqrt2, px, Y0.x), fma(-kRsqrt2, q, Y0.y)};
+    const c64 a1 = {fma(-kRsqrt2, px, Y0.x), fma(kRsqrt2, q, Y0.y)};
+    const double A = Y1.x + Y3.y, B = Y1.y + Y3.x, C = Y1.y - Y3.x, E = Y1.x - Y3.y;
+    const double P1 = fma(kTan8, E, C), P2 = fma(kTan8, B, -A);
+    const double P3 = fma(kTan8, A, B), P4 = fma(kTan8, C, -E);
+    o[3] = {fma(kCos8, P1, a0.x), fma(kCos8, P2, a0.y)};
+    o[11] = {fma(-kCos8, P1, a0.x), fma(-kCos8, P2, a0.y)};
+    o[7] = {fma(kCos8, P4, a1.x), fma(-kCos8, P3, a1.y)};
+    o[15] = {fma(-kCos8, P4, a1.x), fma(kCos8, P3, a1.y)};
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = kInverse ? c64{o[k].y, o[k].x} : o[k];
+}
+
 // T[k] = base * w^k, k = 0..15, applied in place (tree of depth 4 from
 // base, w, w^2, w^4, w^8; a few ulp, inside the rounding margin measured by
 // tests/native/fft_emul.cpp).  kConj multiplies by the conjugates.
@@ -157,13 +222,12 @@ CVM_HD void apply_pow16(c64 v[16], c64 base, c64 w) {
 struct TwBasesW {
   c64 base, w;
 };
-
 // ---------------------------------------------------------------- forward --
 // Input v[a] = p_{t+32a} + i p_{t+32a+512} (untwisted).
 CVM_HD void wfwd_twist_dft(c64 v[16]) {
 #pragma unroll
   for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], twist32(a));
-  dft16<false>(v);
+  dft16f<false>(v);
 }
 CVM_HD void wfwd_stage1(c64 v[16], const TwBasesW& b) {
   wfwd_twist_dft(v);
@@ -201,12 +265,12 @@ CVM_HD void wfwd_stage2a(c64 v[16], int e) {
   }
 }
 // Stage 2b (after the swap put the partner's half in slots 8..15).
-CVM_HD void wfwd_stage2b(c64 v[16]) { dft16<false>(v); }
+CVM_HD void wfwd_stage2b(c64 v[16]) { dft16f<false>(v); }
 
 // ---------------------------------------------------------------- inverse --
 // Mirror image: stage 2b^-1, swap slots 8..15 back (caller), stage 2a^-1,
 // transpose, stage 1^-1.  Output v[a] = M * (p_{t+32a} + i p_{t+32a+512}).
-CVM_HD void winv_stage2b(c64 v[16]) { dft16<true>(v); }
+CVM_HD void winv_stage2b(c64 v[16]) { dft16f<true>(v); }
 CVM_HD void winv_stage2a(c64 v[16], int e) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -220,7 +284,7 @@ CVM_HD void winv_stage2a(c64 v[16], int e) {
   }
 }
 CVM_HD void winv_dft_untwist(c64 v[16]) {
-  dft16<true>(v);
+  dft16f<true>(v);
 #pragma unroll
   for (int a = 1; a < 16; ++a) v[a] = cmul_conj(v[a], twist32(a));
 }
