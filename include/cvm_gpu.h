@@ -140,25 +140,20 @@ CVM_API int cvm_ctx_event_elapsed_ms(cvm_ctx* ctx, double* ms);
  * of the blind-rotation kernel) and its SM count. */
 CVM_API int cvm_ctx_fp64_peak(cvm_ctx* ctx, int reps, double* tflops);
 CVM_API int cvm_ctx_sm_count(cvm_ctx* ctx, int* sms);
-/* Blind-rotation kernel variant (process-wide): 1 = one bootstrap per CTA with
- * the key read through L1; 10*G+S = G bootstraps per CTA sharing an S-stage
- * bulk-copy shared-memory key ring (13, 22, 23, 43); 3044 = four bootstraps
- * per CTA, two transforms in flight per thread; 4044 = 3044 with the key
- * ring in tensor memory (tcgen05.cp / tcgen05.ld); 5044 / 5054 / 5063 =
- * 3044 (G=4, 5) / v2 G=6 with per-thread twiddles generated on use (12
- * resident registers instead of 64); 5144 / 5146 = 5044 plus the rotated
- * accumulator differences held across the gadget levels (4- / 6-row key
- * ring); 5244 / 5245 / 5246 / 5247 = 5144 with each key slot refilled by its
- * last reader (4- to 7-row ring); 9 = one bootstrap on 384 threads (six
- * gadget rows concurrently, latency); 19 = 9 with generated twiddles; 92 = one
- * bootstrap on a 2-SM thread-block cluster; 96 = 92 with the partial
- * products exchanged by st.async + mbarrier instead of a cluster barrier;
- * 6000 + 100*(1-hold) + 10*W + S
- * (W = 1..8, S = 4/5; e.g. 6085) = v4, one bootstrap per warp on a warp-wide
- * FFT, W warps per CTA on an S-row key ring.  0 = auto (default): 96 for
- * levels up to 74 bootstraps, 9 up to 296, else full v4 waves
- * (6085) with the remainder on the cheapest mix of one v4 wave, 5247 rounds
- * and 9 rounds.  Every variant computes bit-identical ciphertexts. */
+/* Blind-rotation kernel variant (process-wide default; a context may
+ * override it, cvm_ctx_set_kernels).  Every variant computes bit-identical
+ * ciphertexts:
+ *   6000 + 10*W + 5 (W = 1..8; 6085 = 8 warps): v4, one bootstrap per warp on
+ *        the warp-wide FFT, W warps per CTA sharing a 5-row key ring
+ *        (throughput; full waves of wide levels);
+ *   5247: v3, four bootstraps per CTA on the 64-thread FFT, 7-row key ring
+ *        (remainder rounds of wide levels);
+ *   9:   one bootstrap per SM, the six gadget rows transformed concurrently;
+ *   96:  one bootstrap per 2-SM thread-block cluster, partial products
+ *        exchanged by st.async (latency: levels up to 74 bootstraps);
+ *   0:   auto (default): 96 up to 74 bootstraps, 9 up to 296, else full v4
+ *        waves with the remainder on the cheapest mix of one v4 wave, 5247
+ *        rounds and 9 rounds. */
 CVM_API int cvm_set_br_variant(int variant);
 CVM_API int cvm_get_br_variant(void);
 /* Wave packing of the levelizer (process-wide, default 1; env CVM_PACK=0):
@@ -168,14 +163,20 @@ CVM_API int cvm_get_br_variant(void);
  * efficiently.  Results are unchanged (gates are pure); 0 = plain levels. */
 CVM_API int cvm_set_level_packing(int on);
 CVM_API int cvm_get_level_packing(void);
-/* Key-switch kernel variant: 1 = one gate per CTA; 6 = one gate on 948
- * threads (6 position groups, latency); 7 = the level as one INT8
- * tensor-core product (one-hot digits x KSK byte limbs) on mma.sync; 8 = the
- * same product on tcgen05.mma with the limb accumulators in tensor memory;
- * 9 = 8 split along the coefficients over up to 16 CTAs per tile plus a
- * reduction; 0 = auto (default: 9).  Bit-identical. */
+/* Key-switch kernel variant (process-wide default): 8 = the level as one
+ * INT8 tcgen05.mma product (one-hot digits x KSK byte limbs, TMEM
+ * accumulators), one CTA per 128-gate x 128-column tile; 9 = the same tiles
+ * split along K into up to 16 CTAs plus a reduction; 0 = auto (9).
+ * Bit-identical. */
 CVM_API int cvm_set_ks_variant(int variant);
 CVM_API int cvm_get_ks_variant(void);
+/* Per-context kernel choices: a blind-rotation variant, a key-switch variant
+ * and wave packing on (1) / off (0); -1 follows the process-wide setting
+ * (the default for a new context).  Invalid values -> CVM_E_INPUT. */
+CVM_API int cvm_ctx_set_kernels(cvm_ctx* ctx, int br_variant, int ks_variant,
+                                int level_packing);
+CVM_API int cvm_ctx_get_kernels(cvm_ctx* ctx, int* br_variant, int* ks_variant,
+                                int* level_packing);
 
 /* ------------------------------------------------------------------------
  * Backend: the cryptovm::Backend contract (gates.hpp:109-132) over a context.

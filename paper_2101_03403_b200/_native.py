@@ -110,6 +110,8 @@ _SIGS = {
     "cvm_get_level_packing": (_i, []),
     "cvm_set_ks_variant": (_i, [_i]),
     "cvm_get_ks_variant": (_i, []),
+    "cvm_ctx_set_kernels": (_i, [_p, _i, _i, _i]),
+    "cvm_ctx_get_kernels": (_i, [_p, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "cvm_backend_create":(_i, [_p, _p, _u64, ctypes.POINTER(_p)]),
     "cvm_backend_destroy": (None, [_p]),
     "cvm_backend_constant": (_i, [_p, _i, _u64p]),

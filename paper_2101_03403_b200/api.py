@@ -214,6 +214,15 @@ class Context:
         check(lib.cvm_ctx_sm_count(self._h, ctypes.byref(v)))
         return v.value
 
+    def set_kernels(self, br_variant=-1, ks_variant=-1, level_packing=-1):
+        """This context's kernel choices (-1 = follow the process-wide setting)."""
+        check(lib.cvm_ctx_set_kernels(self._h, br_variant, ks_variant, level_packing))
+
+    def kernels(self):
+        b, k, p = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib.cvm_ctx_get_kernels(self._h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(p)))
+        return {"br_variant": b.value, "ks_variant": k.value, "level_packing": p.value}
+
     def event(self, which):
         check(lib.cvm_ctx_event_record(self._h, which))
 

@@ -267,7 +267,8 @@ void set_level_packing(bool on) { g_pack.store(on ? 1 : 0); }
 std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(const std::vector<Bit>& ids) const {
   uint32_t depth = 0;
   for (Bit id : ids) depth = std::max(depth, nodes_[id - 1].level);
-  if (level_packing() && depth > 1 && ids.size() > size_t(kPackMinGates)) return pack_levels(ids, depth);
+  if (context_level_packing(ctx_) && depth > 1 && ids.size() > size_t(kPackMinGates))
+    return pack_levels(ids, depth);
   std::vector<std::vector<cvm_gate>> lv;
   for (Bit id : ids) {
     const Node& n = nodes_[id - 1];

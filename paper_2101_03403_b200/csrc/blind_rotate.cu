@@ -138,80 +138,6 @@ __global__ void __launch_bounds__(64) bk_to_fft_kernel(const uint32_t* __restric
     bkf[((size_t)ir * 8 + k2) * 128 + o * 64 + t] = {v[k2].x * s, v[k2].y * s};
 }
 
-// ---------------------------------------------------------- K1 + K2, v1 --
-// One bootstrap per CTA of 64 threads; the key row is read through L1.
-__global__ void __launch_bounds__(64) blind_rotate_kernel(
-    const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
-    const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
-    uint32_t* __restrict__ xout) {
-  __shared__ uint32_t acc[2][kPolyN];
-  __shared__ c64 xbuf[2][512];
-  __shared__ uint16_t bar[kLweWords + 1];
-  const int t = threadIdx.x;
-  const BrJob job = jobs[blockIdx.x];
-  c64 T1[8], T2[8];
-  load_twiddles(tw1, tw2, t, T1, T2);
-  prologue(job, slab, bar, acc[0], acc[1], t, 64, cta_sync, 0);
-  auto sync = [] { __syncthreads(); };
-
-  for (int i = 0; i < kN; ++i) {
-    __syncthreads();
-    const int ai = bar[i];
-    if (ai == 0) continue;  // X^0 - 1 = 0: the CMux leaves ACC unchanged
-    const c64* bk_i = bkf + (size_t)i * kBkfComplexPerStep;
-    c64 af[2][8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      uint32_t dif[16];
-      rotated_diff(acc[part], ai, t, dif);
-#pragma unroll 1
-      for (int p = 0; p < kL; ++p) {
-        c64 v[8];
-        digits(dif, 32 - (p + 1) * kBgBit, v);
-        fwd_stage1(v, T1);
-        exchange<1>(v, xbuf[0], t, sync);
-        fwd_stage2(v, T2);
-        exchange<2>(v, xbuf[1], t, sync);
-        fwd_stage3(v);
-        const c64* bk_r = bk_i + (size_t)(part * kL + p) * 1024;
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          af[0][k2] = cmac(af[0][k2], v[k2], ldg_c64(bk_r + k2 * 128 + t));
-          af[1][k2] = cmac(af[1][k2], v[k2], ldg_c64(bk_r + k2 * 128 + 64 + t));
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      inv_stageA(af[o]);
-      exchange<2>(af[o], xbuf[0], t, sync);
-      inv_stageB(af[o], T2);
-      exchange<3>(af[o], xbuf[1], t, sync);
-      inv_stageC(af[o], T1);
-      add_rounded(acc[o], af[o], t);
-    }
-  }
-  __syncthreads();
-  extract(acc[0], acc[1], xout + (size_t)job.out * kXlweStride, t, 64);
-}
-
-// ---------------------------------------------------------- K1 + K2, v2 --
-// G bootstraps per CTA (64 threads each, independent named barriers); the
-// bootstrapping key is streamed through a ring of S shared-memory stages by
-// the bulk-copy engine, one 16 KB TRGSW row (both output polynomials, all 512
-// bins) per stage, consumed by all G gates.  mbarrier "full" (tx count) /
-// "empty" (64*G arrivals) pairs order the ring; thread 0 is the producer.
-template <int G, int S>
-struct BrSmem2 {
-  c64 ring[S][1024];
-  c64 xbuf[G][2][512];
-  uint32_t acc[G][2][kPolyN];
-  uint16_t bar[G][kLweWords + 1];
-  uint64_t full[S], empty[S];
-};
-
 // Resident bases of the generated twiddles (kTwRec): T1[k] = t1b * t1w^k,
 // T2[k] = t2w^k (see TwPow8).
 struct TwBases {
@@ -228,101 +154,6 @@ __device__ __forceinline__ TwBases tw_bases(const c64* tw1, int t) {
   return b;
 }
 
-template <int G, int S, bool kTwRec = false>
-__global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v2(
-    const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
-    const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
-    uint32_t* __restrict__ xout) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  BrSmem2<G, S>& sm = *reinterpret_cast<BrSmem2<G, S>*>(smem_raw);
-  const int tid = threadIdx.x;
-  const int g = tid >> 6, t = tid & 63;
-  const int bar_id = 1 + g;
-  const int jidx = blockIdx.x * G + g;
-  const bool live = jidx < count;  // idle groups of a partial CTA compute job 0
-  const BrJob job = jobs[live ? jidx : 0];
-  constexpr int kChunks = kN * kRows;
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 64 * G);
-    }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int q = 0; q < S - 1; ++q) {
-      mbar_expect_tx(&sm.full[q], kRowBytes);
-      bulk_g2s(sm.ring[q], bkf + (size_t)q * 1024, kRowBytes, &sm.full[q]);
-    }
-  }
-  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
-  TwBases tb{};
-  if constexpr (kTwRec) tb = tw_bases(tw1, t);
-  else load_twiddles(tw1, tw2, t, T1, T2);
-  uint32_t* acc0 = sm.acc[g][0];
-  uint32_t* acc1 = sm.acc[g][1];
-  uint16_t* bar = sm.bar[g];
-  prologue(job, slab, bar, acc0, acc1, t, 64, group_sync, bar_id);
-  auto sync = [bar_id] { group_sync(bar_id); };
-
-  int q = 0;  // chunk sequence number = i * 6 + row
-  for (int i = 0; i < kN; ++i) {
-    group_sync(bar_id);
-    const int ai = bar[i];
-    c64 af[2][8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      uint32_t dif[16];
-      rotated_diff(part ? acc1 : acc0, ai, t, dif);
-#pragma unroll 1
-      for (int p = 0; p < kL; ++p, ++q) {
-        c64 v[8];
-        digits(dif, 32 - (p + 1) * kBgBit, v);
-        if constexpr (kTwRec) fwd_stage1(v, TwPow8(tb.t1b, tb.t1w));
-        else fwd_stage1(v, T1);
-        exchange<1>(v, sm.xbuf[g][0], t, sync);
-        if constexpr (kTwRec) fwd_stage2(v, TwPow8(tb.t2w));
-        else fwd_stage2(v, T2);
-        exchange<2>(v, sm.xbuf[g][1], t, sync);
-        fwd_stage3(v);
-        // producer: refill the slot chunk q-1 used with chunk q+S-1
-        if (tid == 0 && q + S - 1 < kChunks) {
-          const int nq = q + S - 1, slot = nq % S;
-          if (q >= 1) mbar_wait(&sm.empty[slot], ((q - 1) / S) & 1);
-          mbar_expect_tx(&sm.full[slot], kRowBytes);
-          bulk_g2s(sm.ring[slot], bkf + (size_t)nq * 1024, kRowBytes, &sm.full[slot]);
-        }
-        const int slot = q % S;
-        mbar_wait(&sm.full[slot], (q / S) & 1);
-        const c64* bk_r = sm.ring[slot];
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          af[0][k2] = cmac(af[0][k2], v[k2], bk_r[k2 * 128 + t]);
-          af[1][k2] = cmac(af[1][k2], v[k2], bk_r[k2 * 128 + 64 + t]);
-        }
-        mbar_arrive(&sm.empty[slot]);
-      }
-    }
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      inv_stageA(af[o]);
-      exchange<2>(af[o], sm.xbuf[g][0], t, sync);
-      if constexpr (kTwRec) inv_stageB(af[o], TwPow8(tb.t2w));
-      else inv_stageB(af[o], T2);
-      exchange<3>(af[o], sm.xbuf[g][1], t, sync);
-      if constexpr (kTwRec) inv_stageC(af[o], TwPow8(tb.t1b, tb.t1w));
-      else inv_stageC(af[o], T1);
-      add_rounded(o ? acc1 : acc0, af[o], t);
-    }
-  }
-  group_sync(bar_id);
-  if (live) extract(acc0, acc1, xout + (size_t)job.out * kXlweStride, t, 64);
-}
-
 // ---------------------------------------------------------- K1 + K2, v3 --
 // As v2, but every thread runs two transforms at once: the forward FFTs of
 // the same gadget level of both TRLWE parts (rows p and 3+p), and the two
@@ -336,10 +167,8 @@ struct BrSmem3 {
   c64 xbuf[G][2][512];
   uint32_t acc[G][2][kPolyN];
   uint16_t bar[G][kLweWords + 1];
-  uint64_t full[S], empty[S];
-  uint64_t tfull[S], tempty[S];  // TMEM key ring (kTmem)
-  uint32_t cnt[S];               // readers done with each slot (kLast)
-  uint32_t tmem_base;
+  uint64_t full[S];
+  uint32_t cnt[S];  // readers done with each slot
 };
 
 // chunk q (0 .. 6n-1, pair order) -> TRGSW row in the FFT-domain key
@@ -349,22 +178,16 @@ __device__ __forceinline__ const c64* chunk_src(const c64* bkf, int q) {
   return bkf + ((size_t)i * kRows + row) * 1024;
 }
 
-// kTmem: the key rows are copied once per CTA from the shared-memory ring
-// into a tensor-memory ring (tcgen05.cp, 64 columns per row, each thread's
-// bins in its own lane) and every bootstrap reads them with tcgen05.ld --
-// the G-fold shared-memory key reads leave the LSU path.  Thread 0 stages:
-// TMA row c -> smem slot c%4 -> (after the consumers released TMEM slot c%4)
-// tcgen05.cp -> commit on tfull[c%4]; consumers release via tempty.
-// kTwRec: twiddles generated on use (TwPow8) -- 12 resident registers
-// instead of 64, so five bootstraps (10 warps) fit an SM's register file.
-template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false,
-          bool kLast = false>
+// The remainder kernel of wide levels (variant 5247: G = 4 bootstraps per
+// CTA on a 7-row ring): twiddles generated on use (TwPow8, 12 resident
+// registers instead of 64), the rotated accumulator differences held across
+// the three gadget levels, and each key slot refilled by its last reader.
+template <int G, int S>
 __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
     const BrJob* __restrict__ jobs, int count, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
     uint32_t* __restrict__ xout) {
   static_assert(S >= 4, "pairs need two chunks in flight plus prefetch");
-  static_assert(!kTmem || S == 4, "the TMEM ring mirrors a 4-slot smem ring");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BrSmem3<G, S>& sm = *reinterpret_cast<BrSmem3<G, S>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -374,67 +197,24 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
   const bool live = jidx < count;
   const BrJob job = jobs[live ? jidx : 0];
   constexpr int kChunks = kN * kRows;
-  constexpr uint32_t kTmemCols = 64 * 4;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 64 * G);
-      mbar_init(&sm.tfull[s], 1);
-      mbar_init(&sm.tempty[s], 64 * G);
       sm.cnt[s] = 0;
     }
     mbar_init_fence();
   }
-  if constexpr (kTmem) {
-    if (tid < 32) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(&sm.tmem_base)),
-                   "r"(kTmemCols)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-  }
   __syncthreads();
-  uint32_t tbase = 0, tlane = 0;
-  if constexpr (kTmem) {
-    tc_fence_after();
-    tbase = sm.tmem_base;
-    tlane = uint32_t(32 * ((tid >> 5) & 3)) << 16;  // this warp's lane quarter
-  }
-  // thread 0: copy staged row c (smem slot c%4) into TMEM slot c%4
-  auto stage_tmem = [&](int c) {
-    const int s = c & 3;
-    if (c >= 4) mbar_wait(&sm.tempty[s], ((c - 4) >> 2) & 1);
-    mbar_wait(&sm.full[s], (c >> 2) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int blk = 0; blk < 16; ++blk)
-      tc_cp_64x128_0213(tbase + uint32_t(s * 64 + blk * 4),
-                        smem_desc_rows16(&sm.ring[s][blk * 64]));
-    tc_commit(&sm.tfull[s]);
-  };
   if (tid == 0) {
     for (int q = 0; q < S; ++q) {
       mbar_expect_tx(&sm.full[q], kRowBytes);
       bulk_g2s(sm.ring[q], chunk_src(bkf, q), kRowBytes, &sm.full[q]);
     }
-    if constexpr (kTmem) {
-      stage_tmem(0);
-      stage_tmem(1);
-    }
   }
-  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
-  c64 t1b{}, t1w{}, t2w{};  // kTwRec: T1[k] = t1b * t1w^k, T2[k] = t2w^k
-  if constexpr (!kTwRec) {
-    load_twiddles(tw1, tw2, t, T1, T2);
-  } else {
-    const TwBases b = tw_bases(tw1, t);
-    t1b = b.t1b;
-    t1w = b.t1w;
-    t2w = b.t2w;
-  }
+  // T1[k] = t1b * t1w^k, T2[k] = t2w^k
+  const TwBases twb = tw_bases(tw1, t);
+  const c64 t1b = twb.t1b, t1w = twb.t1w, t2w = twb.t2w;
   uint32_t* acc0 = sm.acc[g][0];
   uint32_t* acc1 = sm.acc[g][1];
   uint16_t* bar = sm.bar[g];
@@ -450,7 +230,7 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
 #pragma unroll
     for (int k = 0; k < 8; ++k) af[0][k] = af[1][k] = c64{0.0, 0.0};
     // (X^ai - 1) * ACC at coefficients j and j + 512 of both parts, offset
-    // for the decomposition; kHold keeps the 32 words for the three gadget
+    // for the decomposition; the 32 words are kept for the three gadget
     // levels instead of re-reading the accumulator per level
     auto rot_diff = [&](int x, uint32_t& da0, uint32_t& da1, uint32_t& db0, uint32_t& db1) {
       const int j = t + 64 * x;
@@ -465,167 +245,84 @@ __global__ void __launch_bounds__(64 * G, 1) blind_rotate_kernel_v3(
       db0 = rb0 - acc1[j] + kDecompOffset;
       db1 = rb1 - acc1[j + 512] + kDecompOffset;
     };
-    uint32_t dh[kHold ? 8 : 1][4];
-    if constexpr (kHold) {
+    uint32_t dh[8][4];
 #pragma unroll
-      for (int x = 0; x < 8; ++x) rot_diff(x, dh[x][0], dh[x][1], dh[x][2], dh[x][3]);
-    }
+    for (int x = 0; x < 8; ++x) rot_diff(x, dh[x][0], dh[x][1], dh[x][2], dh[x][3]);
 #pragma unroll 1
     for (int p = 0; p < kL; ++p, q += 2) {
       const int shift = 32 - (p + 1) * kBgBit;
       c64 va[8], vb[8];
 #pragma unroll
       for (int x = 0; x < 8; ++x) {
-        uint32_t da0, da1, db0, db1;
-        if constexpr (kHold) {
-          da0 = dh[x][0];
-          da1 = dh[x][1];
-          db0 = dh[x][2];
-          db1 = dh[x][3];
-        } else {
-          rot_diff(x, da0, da1, db0, db1);
-        }
+        const uint32_t da0 = dh[x][0], da1 = dh[x][1], db0 = dh[x][2], db1 = dh[x][3];
         va[x] = {u32_biased_to_double((da0 >> shift) & 127u, kDigitBias),
                  u32_biased_to_double((da1 >> shift) & 127u, kDigitBias)};
         vb[x] = {u32_biased_to_double((db0 >> shift) & 127u, kDigitBias),
                  u32_biased_to_double((db1 >> shift) & 127u, kDigitBias)};
       }
-      if constexpr (kTwRec) {
+      {
         const TwPow8 w1(t1b, t1w);
         fwd_stage1(va, w1);
         fwd_stage1(vb, w1);
-      } else {
-        fwd_stage1(va, T1);
-        fwd_stage1(vb, T1);
       }
       exchange_pair<1>(va, vb, xa, xb, t, bar_id);
-      if constexpr (kTwRec) {
+      {
         const TwPow8 w2(t2w);
         fwd_stage2(va, w2);
         fwd_stage2(vb, w2);
-      } else {
-        fwd_stage2(va, T2);
-        fwd_stage2(vb, T2);
       }
       exchange_pair<2>(va, vb, xa, xb, t, bar_id);
       fwd_stage3(va);
       fwd_stage3(vb);
       const int sa = q % S, sb = (q + 1) % S;
-      if constexpr (!kTmem) {
-        // producer: refill the slots of chunks q-2, q-1 with chunks q+S-2, q+S-1
-        // (kLast: the last consumer of a slot refills it instead, below)
-        if (!kLast && tid == 0) {
+      mbar_wait(&sm.full[sa], (q / S) & 1);
+      mbar_wait(&sm.full[sb], ((q + 1) / S) & 1);
+      const c64* bka = sm.ring[sa];
+      const c64* bkb = sm.ring[sb];
 #pragma unroll
-          for (int c = q - 2; c < q; ++c) {
-            if (c < 0 || c + S >= kChunks) continue;
-            const int slot = c % S;
-            mbar_wait(&sm.empty[slot], (c / S) & 1);
-            mbar_expect_tx(&sm.full[slot], kRowBytes);
-            bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
-          }
-        }
-        mbar_wait(&sm.full[sa], (q / S) & 1);
-        mbar_wait(&sm.full[sb], ((q + 1) / S) & 1);
-        const c64* bka = sm.ring[sa];
-        const c64* bkb = sm.ring[sb];
+      for (int k2 = 0; k2 < 8; ++k2) {
+        const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
+        const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
+        af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
+        af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
+      }
+      // the slot's last reader (counted per warp) streams the chunk S ahead
+      // into it at once, so no thread blocks waiting for the slowest bootstrap
+      __syncwarp();
+      if ((tid & 31) == 0) {
+        __threadfence_block();
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          const c64 a0 = bka[k2 * 128 + t], a1 = bka[k2 * 128 + 64 + t];
-          const c64 b0 = bkb[k2 * 128 + t], b1 = bkb[k2 * 128 + 64 + t];
-          af[0][k2] = cmac(cmac(af[0][k2], va[k2], a0), vb[k2], b0);
-          af[1][k2] = cmac(cmac(af[1][k2], va[k2], a1), vb[k2], b1);
-        }
-        if constexpr (!kLast) {
-          mbar_arrive(&sm.empty[sa]);
-          mbar_arrive(&sm.empty[sb]);
-        } else {
-          // the slot's last reader (counted per warp) streams the chunk S
-          // ahead into it at once, so no thread blocks waiting for the
-          // slowest bootstrap
-          __syncwarp();
-          if ((tid & 31) == 0) {
-            __threadfence_block();
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int slot = h ? sb : sa, c = q + h;
-              if (atomicAdd(&sm.cnt[slot], 32u) == 64u * G - 32u) {
-                sm.cnt[slot] = 0;
-                if (c + S < kChunks) {
-                  mbar_expect_tx(&sm.full[slot], kRowBytes);
-                  bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
-                }
-              }
+        for (int h = 0; h < 2; ++h) {
+          const int slot = h ? sb : sa, c = q + h;
+          if (atomicAdd(&sm.cnt[slot], 32u) == 64u * G - 32u) {
+            sm.cnt[slot] = 0;
+            if (c + S < kChunks) {
+              mbar_expect_tx(&sm.full[slot], kRowBytes);
+              bulk_g2s(sm.ring[slot], chunk_src(bkf, c + S), kRowBytes, &sm.full[slot]);
             }
           }
-        }
-      } else {
-        mbar_wait(&sm.tfull[sa], (q >> 2) & 1);
-        mbar_wait(&sm.tfull[sb], ((q + 1) >> 2) & 1);
-        tc_fence_after();
-        const uint32_t ta = tbase + tlane + uint32_t(sa * 64);
-        const uint32_t tb = tbase + tlane + uint32_t(sb * 64);
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          uint32_t ra[8], rb[8];
-          tc_ld8(ta + uint32_t(k2 * 8), ra);  // (k2, o = 0, 1) of row a
-          tc_ld8(tb + uint32_t(k2 * 8), rb);
-          tc_wait_ld16(ra, rb);
-          af[0][k2] = cmac(cmac(af[0][k2], va[k2], c64_of(ra)), vb[k2], c64_of(rb));
-          af[1][k2] = cmac(cmac(af[1][k2], va[k2], c64_of(ra + 4)), vb[k2], c64_of(rb + 4));
-        }
-        tc_fence_before();
-        mbar_arrive(&sm.tempty[sa]);
-        mbar_arrive(&sm.tempty[sb]);
-        if (tid == 0) {
-          // smem slots of chunks q, q+1 were read by their (completed) copies:
-          // stream chunks q+4, q+5 into them; then copy chunks q+2, q+3
-          // (staged one pair ago) into TMEM slots freed by chunks q-2, q-1
-#pragma unroll
-          for (int c = q + 4; c < q + 6; ++c) {
-            if (c >= kChunks) continue;
-            mbar_expect_tx(&sm.full[c & 3], kRowBytes);
-            bulk_g2s(sm.ring[c & 3], chunk_src(bkf, c), kRowBytes, &sm.full[c & 3]);
-          }
-          if (q + 2 < kChunks) stage_tmem(q + 2);
-          if (q + 3 < kChunks) stage_tmem(q + 3);
         }
       }
     }
     inv_stageA(af[0]);
     inv_stageA(af[1]);
     exchange_pair<2>(af[0], af[1], xa, xb, t, bar_id);
-    if constexpr (kTwRec) {
+    {
       const TwPow8 w2(t2w);
       inv_stageB(af[0], w2);
       inv_stageB(af[1], w2);
-    } else {
-      inv_stageB(af[0], T2);
-      inv_stageB(af[1], T2);
     }
     exchange_pair<3>(af[0], af[1], xa, xb, t, bar_id);
-    if constexpr (kTwRec) {
+    {
       const TwPow8 w1(t1b, t1w);
       inv_stageC(af[0], w1);
       inv_stageC(af[1], w1);
-    } else {
-      inv_stageC(af[0], T1);
-      inv_stageC(af[1], T1);
     }
     add_rounded(acc0, af[0], t);
     add_rounded(acc1, af[1], t);
   }
   group_sync(bar_id);
   if (live) extract(acc0, acc1, xout + (size_t)job.out * kXlweStride, t, 64);
-  if constexpr (kTmem) {
-    tc_fence_before();
-    __syncthreads();
-    if (tid < 32) {
-      tc_fence_after();
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                   "r"(kTmemCols)
-                   : "memory");
-    }
-  }
 }
 
 // ------------------------------------------------ K1 + K2, latency: wide --
@@ -645,7 +342,6 @@ struct WideSmem {
   uint64_t full[kRows];
 };
 
-template <bool kTwRec>
 __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
     const c64* __restrict__ bkf, const c64* __restrict__ tw1, const c64* __restrict__ tw2,
@@ -667,10 +363,8 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     mbar_expect_tx(&sm.full[g], kRowBytes);
     bulk_g2s(sm.bkbuf[g], bkf + (size_t)g * 1024, kRowBytes, &sm.full[g]);
   }
-  c64 T1[kTwRec ? 1 : 8], T2[kTwRec ? 1 : 8];
-  TwBases tb{};
-  if constexpr (kTwRec) tb = tw_bases(tw1, t);
-  else load_twiddles(tw1, tw2, t, T1, T2);
+  c64 T1[8], T2[8];
+  load_twiddles(tw1, tw2, t, T1, T2);
   prologue(job, slab, sm.bar, sm.acc[0], sm.acc[1], tid, 64 * kRows, cta_sync, 0);
   const int shift = 32 - (p + 1) * kBgBit;
   c64* xb = sm.xbuf[g];
@@ -683,12 +377,10 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
     rotated_diff(sm.acc[part], ai, t, dif);
     c64 v[8];
     digits(dif, shift, v);
-    if constexpr (kTwRec) fwd_stage1(v, TwPow8(tb.t1b, tb.t1w));
-    else fwd_stage1(v, T1);
+    fwd_stage1(v, T1);
     exchange<1>(v, xb, t, sync);
     group_sync(bar_id);  // WAR on the single exchange buffer
-    if constexpr (kTwRec) fwd_stage2(v, TwPow8(tb.t2w));
-    else fwd_stage2(v, T2);
+    fwd_stage2(v, T2);
     exchange<2>(v, xb, t, sync);
     fwd_stage3(v);
     // partial products of this row with both output polynomials
@@ -729,11 +421,9 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
         v[k2] = cadd(cadd(sm.red[0][o][k2][t], sm.red[1][o][k2][t]), sm.red[2][o][k2][t]);
       inv_stageA(v);
       exchange<2>(v, sm.xbuf[g], t, sync);
-      if constexpr (kTwRec) inv_stageB(v, TwPow8(tb.t2w));
-      else inv_stageB(v, T2);
+      inv_stageB(v, T2);
       exchange<3>(v, sm.xbuf[g + 2], t, sync);
-      if constexpr (kTwRec) inv_stageC(v, TwPow8(tb.t1b, tb.t1w));
-      else inv_stageC(v, T1);
+      inv_stageC(v, T1);
       add_rounded(sm.acc[o], v, t);
     }
   }
@@ -759,17 +449,16 @@ struct PairSmem {
   uint32_t acc[kPolyN];   // ACC part r
   uint16_t bar[kLweWords + 1];
   uint64_t full[kL];
-  uint64_t rbar[2];  // kAsync: the peer's partial of step parity 0 / 1 landed
+  uint64_t rbar[2];  // the peer's partial of step parity 0 / 1 landed
 };
 
-// kAsync: the peer's partial product arrives by st.async remote stores that
+// The peer's partial product arrives by st.async remote stores that
 // complete a transaction count on this CTA's rbar mbarrier (armed each step
 // with the expected 8 KB), so the consumer waits on a local mbarrier instead
 // of a cluster barrier (whose release fence, MEMBAR.ALL.GPU, and
 // arrive/wait were ~15% of the pair kernel's stall samples).  The receive
 // buffer alternates by step parity; the data dependence through the two
 // accumulator parts keeps the peer from overwriting a buffer still being read.
-template <bool kAsync = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     blind_rotate_pair_kernel(const BrJob* __restrict__ jobs, const uint32_t* __restrict__ slab,
                              const c64* __restrict__ bkf, const c64* __restrict__ tw1,
@@ -811,16 +500,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     for (int j = tid; j < kPolyN; j += 64 * kL)
       sm.acc[j] = r == 0 ? 0u : ((((j + barb) & (2 * kPolyN - 1)) < kPolyN) ? kMu : (0u - kMu));
   }
-  c64* peer_recv = cluster.map_shared_rank(&sm.recv[0][0][0], r ^ 1);
-  uint32_t peer_recv_a = 0, peer_rbar_a = 0;  // shared::cluster addresses in the peer
-  if constexpr (kAsync) {
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                 : "=r"(peer_recv_a)
-                 : "r"(smem_u32(&sm.recv[0][0][0])), "r"(r ^ 1));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                 : "=r"(peer_rbar_a)
-                 : "r"(smem_u32(&sm.rbar[0])), "r"(r ^ 1));
-  }
+  uint32_t peer_recv_a, peer_rbar_a;  // shared::cluster addresses in the peer
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(peer_recv_a)
+               : "r"(smem_u32(&sm.recv[0][0][0])), "r"(r ^ 1));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(peer_rbar_a)
+               : "r"(smem_u32(&sm.rbar[0])), "r"(r ^ 1));
   const int shift = 32 - (g + 1) * kBgBit;
   c64* xb0 = sm.xbuf[g][0];
   c64* xb1 = sm.xbuf[g][1];
@@ -829,7 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
 
   for (int i = 0; i < kN; ++i) {
     __syncthreads();  // ACC part r of the previous step complete
-    if (kAsync && tid == 0) mbar_expect_tx(&sm.rbar[i & 1], 8 * 64 * 16);
+    if (tid == 0) mbar_expect_tx(&sm.rbar[i & 1], 8 * 64 * 16);
     const int ai = sm.bar[i];
     uint32_t dif[16];
     rotated_diff(sm.acc, ai, t, dif);
@@ -855,33 +541,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
     }
     __syncthreads();  // all three levels' partial products in red
     if (g == 1) {     // the peer's polynomial: sum over levels, store remotely
-      c64* dst = peer_recv + (i & 1) * 512;
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) {
         const c64 x = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
                            sm.red[2][r ^ 1][k2][t]);
-        if constexpr (kAsync) {
-          const uint32_t a = peer_recv_a + uint32_t(((i & 1) * 512 + k2 * 64 + t) * 16);
-          asm volatile(
-              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, "
-              "[%3];" ::"r"(a),
-              "l"(__double_as_longlong(x.x)), "l"(__double_as_longlong(x.y)),
-              "r"(peer_rbar_a + uint32_t(8 * (i & 1)))
-              : "memory");
-        } else {
-          dst[k2 * 64 + t] = x;
-        }
+        const uint32_t a = peer_recv_a + uint32_t(((i & 1) * 512 + k2 * 64 + t) * 16);
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, "
+            "[%3];" ::"r"(a),
+            "l"(__double_as_longlong(x.x)), "l"(__double_as_longlong(x.y)),
+            "r"(peer_rbar_a + uint32_t(8 * (i & 1)))
+            : "memory");
       }
     } else if (g == 0) {  // my polynomial: local part of the sum
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2)
         v[k2] = cadd(cadd(sm.red[0][r][k2][t], sm.red[1][r][k2][t]), sm.red[2][r][k2][t]);
     }
-    if constexpr (kAsync) {
-      if (g == 0) mbar_wait(&sm.rbar[i & 1], (i >> 1) & 1);  // the peer's partial landed
-    } else {
-      cluster.sync();  // partial products exchanged
-    }
+    if (g == 0) mbar_wait(&sm.rbar[i & 1], (i >> 1) & 1);  // the peer's partial landed
     if (g == 0) {
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) v[k2] = cadd(v[k2], sm.recv[i & 1][k2][t]);
@@ -911,54 +588,37 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
   return cudaGetLastError();
 }
 
-template <int G, int S, bool kTwRec = false>
-static cudaError_t launch_v2(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
-                             const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
-  static std::atomic<uint64_t> configured{0};
-  const int smem = int(sizeof(BrSmem2<G, S>));
-  cudaError_t e = set_smem(blind_rotate_kernel_v2<G, S, kTwRec>, smem, configured);
-  if (e != cudaSuccess) return e;
-  blind_rotate_kernel_v2<G, S, kTwRec><<<(count + G - 1) / G, 64 * G, smem, s>>>(
-      jobs, count, slab, bkf, tw1, tw2, xout);
-  return cudaGetLastError();
-}
-
-template <int G, int S, bool kTmem = false, bool kTwRec = false, bool kHold = false,
-          bool kLast = false>
 static cudaError_t launch_v3(const BrJob* jobs, int count, const uint32_t* slab, const c64* bkf,
                              const c64* tw1, const c64* tw2, uint32_t* xout, cudaStream_t s) {
+  constexpr int G = 4, S = 7;
   static std::atomic<uint64_t> configured{0};
+  auto* kern = blind_rotate_kernel_v3<G, S>;
   const int smem = int(sizeof(BrSmem3<G, S>));
-  auto* kern = blind_rotate_kernel_v3<G, S, kTmem, kTwRec, kHold, kLast>;
   cudaError_t e = set_smem(kern, smem, configured);
   if (e != cudaSuccess) return e;
   kern<<<(count + G - 1) / G, 64 * G, smem, s>>>(jobs, count, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
-template <bool kTwRec = false>
 static cudaError_t launch_wide(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
   static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(WideSmem));
-  cudaError_t e = set_smem(blind_rotate_wide_kernel<kTwRec>, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_wide_kernel, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_wide_kernel<kTwRec><<<count, 64 * kRows, smem, s>>>(jobs, slab, bkf, tw1, tw2,
-                                                                   xout);
+  blind_rotate_wide_kernel<<<count, 64 * kRows, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
-template <bool kAsync = false>
 static cudaError_t launch_pair(const BrJob* jobs, int count, const uint32_t* slab,
                                const c64* bkf, const c64* tw1, const c64* tw2, uint32_t* xout,
                                cudaStream_t s) {
   static std::atomic<uint64_t> configured{0};
   const int smem = int(sizeof(PairSmem));
-  cudaError_t e = set_smem(blind_rotate_pair_kernel<kAsync>, smem, configured);
+  cudaError_t e = set_smem(blind_rotate_pair_kernel, smem, configured);
   if (e != cudaSuccess) return e;
-  blind_rotate_pair_kernel<kAsync><<<2 * count, 64 * kL, smem, s>>>(jobs, slab, bkf, tw1, tw2,
-                                                                   xout);
+  blind_rotate_pair_kernel<<<2 * count, 64 * kL, smem, s>>>(jobs, slab, bkf, tw1, tw2, xout);
   return cudaGetLastError();
 }
 
@@ -970,20 +630,15 @@ int br_variant() {
 void set_br_variant(int v) { g_br_variant = v; }
 int default_br_variant() { return kDefaultBrVariant; }
 bool valid_br_variant(int v) {
-  return v == 0 || v == 1 || v == 9 || v == 19 || v == 92 || v == 96 || v == 13 || v == 22 ||
-         v == 23 ||
-         v == 43 ||
-         v == 3044 || v == 4044 ||
-         v == 5044 || v == 5054 || v == 5063 || v == 5144 || v == 5146 || v == 5244 ||
-         v == 5245 || v == 5246 || v == 5247 || valid_br_v4_variant(v);
+  return v == 0 || v == 9 || v == 96 || v == 5247 || valid_br_v4_variant(v);
 }
 
-cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
+cudaError_t launch_blind_rotate(int variant, const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 const c64* bkf4, const c64* tw4, uint32_t* xout,
                                 cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  int variant = br_variant();
+  if (variant < 0) variant = br_variant();
   if (valid_br_v4_variant(variant))
     return launch_blind_rotate_v4(variant, jobs, count, slab, bkf4, tw4, xout, s);
   if (variant == 0) {
@@ -1023,8 +678,7 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
       }
       if (b4 && done < count) {
         const int n = std::min(count - done, b4 * kW4);
-        cudaError_t e = launch_v3<4, 7, false, true, true, true>(jobs + done, n, slab, bkf, tw1,
-                                                                 tw2, xout, s);
+        cudaError_t e = launch_v3(jobs + done, n, slab, bkf, tw1, tw2, xout, s);
         if (e != cudaSuccess) return e;
         done += n;
       }
@@ -1034,34 +688,9 @@ cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* sl
     }
   }
   switch (variant) {
-    case 1:
-      blind_rotate_kernel<<<count, 64, 0, s>>>(jobs, slab, bkf, tw1, tw2, xout);
-      return cudaGetLastError();
     case 9: return launch_wide(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 19: return launch_wide<true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 92: return launch_pair(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 96: return launch_pair<true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 13: return launch_v2<1, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 22: return launch_v2<2, 2>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 23: return launch_v2<2, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 43: return launch_v2<4, 3>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5063: return launch_v2<6, 3, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 3044: return launch_v3<4, 4>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 4044: return launch_v3<4, 4, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5044: return launch_v3<4, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5054: return launch_v3<5, 4, false, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5144:
-      return launch_v3<4, 4, false, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5146:
-      return launch_v3<4, 6, false, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5244:  // 5144 + the last reader of a key slot refills it
-      return launch_v3<4, 4, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5245:
-      return launch_v3<4, 5, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5246:
-      return launch_v3<4, 6, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
-    case 5247:
-      return launch_v3<4, 7, false, true, true, true>(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 96: return launch_pair(jobs, count, slab, bkf, tw1, tw2, xout, s);
+    case 5247: return launch_v3(jobs, count, slab, bkf, tw1, tw2, xout, s);
     default: return cudaErrorInvalidValue;
   }
 }

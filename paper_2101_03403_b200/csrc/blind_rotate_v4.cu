@@ -277,23 +277,17 @@ static cudaError_t launch_v4(int warps, const BrJob* jobs, int count, const uint
   return cudaGetLastError();
 }
 
-// 6000 + 100 * (1 - hold) + 10 * warps + S, warps = 1..8, S = 4 or 5
+// 6000 + 10 * warps + 5, warps = 1..8 (held digits, 5-row key ring)
 bool valid_br_v4_variant(int v) {
-  const int h = (v / 100) % 10, w = (v / 10) % 10, st = v % 10;
-  return v / 1000 == 6 && h <= 1 && w >= 1 && w <= kV4MaxWarps && (st == 4 || st == 5);
+  const int w = (v - 6005) / 10;
+  return v >= 6015 && v <= 6085 && (v - 6005) % 10 == 0 && w >= 1 && w <= kV4MaxWarps;
 }
 
 cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
                                    const uint32_t* slab, const c64* bkf4, const c64* tw4,
                                    uint32_t* xout, cudaStream_t s) {
   if (!valid_br_v4_variant(variant)) return cudaErrorInvalidValue;
-  const bool hold = (variant / 100) % 10 == 0;
-  const int warps = (variant / 10) % 10, st = variant % 10;
-  if (hold)
-    return st == 5 ? launch_v4<5, true>(warps, jobs, count, slab, bkf4, tw4, xout, s)
-                   : launch_v4<4, true>(warps, jobs, count, slab, bkf4, tw4, xout, s);
-  return st == 5 ? launch_v4<5, false>(warps, jobs, count, slab, bkf4, tw4, xout, s)
-                 : launch_v4<4, false>(warps, jobs, count, slab, bkf4, tw4, xout, s);
+  return launch_v4<5, true>((variant / 10) % 10, jobs, count, slab, bkf4, tw4, xout, s);
 }
 
 }  // namespace cvm

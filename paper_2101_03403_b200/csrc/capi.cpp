@@ -253,6 +253,23 @@ int cvm_set_ks_variant(int v) {
   });
 }
 int cvm_get_ks_variant(void) { return cvm::ks_variant(); }
+int cvm_ctx_set_kernels(cvm_ctx* c, int br_variant, int ks_variant, int level_packing) {
+  return guard([&] {
+    need(c, "ctx");
+    if (br_variant != -1 && !valid_br_variant(br_variant))
+      throw InputError("unknown blind-rotation variant " + std::to_string(br_variant));
+    if (ks_variant != -1 && !valid_ks_variant(ks_variant))
+      throw InputError("unknown key-switch variant " + std::to_string(ks_variant));
+    if (level_packing < -1 || level_packing > 1) throw InputError("level_packing is -1, 0 or 1");
+    context_set_kernels(c->ctx, br_variant, ks_variant, level_packing);
+  });
+}
+int cvm_ctx_get_kernels(cvm_ctx* c, int* br_variant, int* ks_variant, int* level_packing) {
+  return guard([&] {
+    need(c, "ctx");
+    context_get_kernels(c->ctx, br_variant, ks_variant, level_packing);
+  });
+}
 
 // -------------------------------------------------------------- backend --
 int cvm_backend_create(cvm_ctx* c, const cvm_keyset* owner, uint64_t enc_seed,

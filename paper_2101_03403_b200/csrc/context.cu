@@ -112,8 +112,6 @@ class Context {
     cudaFree(tw4_);
     cudaFree(bkf_);
     cudaFree(bkf4_);
-    cudaFree(ksk_);
-    cudaFree(kskb_);
     cudaFree(ksktc_);
     cudaFree(kspart_);
     cudaFree(slab_);
@@ -127,7 +125,8 @@ class Context {
     check(cudaSetDevice(device_), "cudaSetDevice");
     if (!bkf_) check(cudaMalloc(&bkf_, kBkfBytes), "cudaMalloc(bkf)");
     const size_t ksk_rows = size_t(kPolyN) * kKsT * kKsBase;
-    if (!ksk_) check(cudaMalloc(&ksk_, ksk_rows * kKskRowStride * 4), "cudaMalloc(ksk)");
+    uint32_t* ksk_pad = nullptr;  // staging only: the tcgen05 tiles are built from it
+    check(cudaMalloc(&ksk_pad, ksk_rows * kKskRowStride * 4), "cudaMalloc(ksk)");
     uint32_t* bk_tmp = nullptr;
     check(cudaMalloc(&bk_tmp, kBkWords * 4), "cudaMalloc(bk tmp)");
     check(cudaMemcpyAsync(bk_tmp, bk, kBkWords * 4, cudaMemcpyHostToDevice, stream_),
@@ -139,19 +138,17 @@ class Context {
     check(launch_bk_to_fft_v4(bk_tmp, tw4_, bkf4_, stream_), "bk_to_fft_v4");
     ++stats_.other_launches;
     // KSK rows padded 631 -> 632 words (pad word zero)
-    check(cudaMemsetAsync(ksk_, 0, ksk_rows * kKskRowStride * 4, stream_), "memset ksk");
-    check(cudaMemcpy2DAsync(ksk_, kKskRowStride * 4, ksk, kLweWords * 4, kLweWords * 4,
+    check(cudaMemsetAsync(ksk_pad, 0, ksk_rows * kKskRowStride * 4, stream_), "memset ksk");
+    check(cudaMemcpy2DAsync(ksk_pad, kKskRowStride * 4, ksk, kLweWords * 4, kLweWords * 4,
                             ksk_rows, cudaMemcpyHostToDevice, stream_),
           "upload ksk");
-    if (!kskb_) check(cudaMalloc(&kskb_, kKskbWords * 4), "cudaMalloc(kskb)");
-    check(launch_ksk_to_limbs(ksk_, kskb_, stream_), "ksk_to_limbs");
-    ++stats_.other_launches;
     if (!ksktc_) check(cudaMalloc(&ksktc_, kKskTcWords * 4), "cudaMalloc(ksktc)");
     if (!kspart_) check(cudaMalloc(&kspart_, kKsPartWords * 4), "cudaMalloc(kspart)");
-    check(launch_ksk_to_tc(ksk_, ksktc_, stream_), "ksk_to_tc");
+    check(launch_ksk_to_tc(ksk_pad, ksktc_, stream_), "ksk_to_tc");
     ++stats_.other_launches;
     check(cudaStreamSynchronize(stream_), "sync(upload_keys)");
     cudaFree(bk_tmp);
+    cudaFree(ksk_pad);
     has_keys_ = true;
   }
 
@@ -290,12 +287,12 @@ class Context {
 
   void launch_level(const BrJob* d_br, uint64_t n_br, const KsJob* d_ks, uint64_t n_ks) {
     Prof* p = begin_prof(0);
-    check(launch_blind_rotate(d_br, int(n_br), slab_, bkf_, tw1_, tw2_, bkf4_, tw4_, xlwe_,
-                              stream_),
+    check(launch_blind_rotate(br_variant, d_br, int(n_br), slab_, bkf_, tw1_, tw2_, bkf4_, tw4_,
+                              xlwe_, stream_),
           "blind_rotate_kernel");
     end_prof(p);
     p = begin_prof(1);
-    check(launch_key_switch(d_ks, int(n_ks), xlwe_, ksk_, kskb_, ksktc_, kspart_, slab_, stream_),
+    check(launch_key_switch(ks_variant, d_ks, int(n_ks), xlwe_, ksktc_, kspart_, slab_, stream_),
           "key_switch_kernel");
     end_prof(p);
     stats_.br_launches++;
@@ -526,9 +523,7 @@ class Context {
   cudaStream_t stream_ = nullptr;
   c64 *tw1_ = nullptr, *tw2_ = nullptr, *bkf_ = nullptr;
   c64 *tw4_ = nullptr, *bkf4_ = nullptr;  // warp-FFT twiddle bases and key (v4)
-  uint32_t* ksk_ = nullptr;
-  uint32_t* kskb_ = nullptr;   // KSK as byte limbs for the mma.sync key switch
-  uint32_t* ksktc_ = nullptr;  // the same limbs as tcgen05 B tiles
+  uint32_t* ksktc_ = nullptr;  // the KSK's byte limbs as tcgen05 B tiles
   uint32_t* kspart_ = nullptr;  // split-K partials of key-switch variant 9
   uint32_t* slab_ = nullptr;
   uint64_t cap_ = 0;
@@ -551,6 +546,9 @@ class Context {
   // entry point below holds it for its whole call.  The slot
   // allocator has its own lock (alloc_mu_).
   std::recursive_mutex mu;
+  // Kernel choices of this context: -1 follows the process-wide setting
+  // (cvm_set_br_variant / cvm_set_ks_variant / cvm_set_level_packing).
+  int br_variant = -1, ks_variant = -1, level_packing = -1;
 };
 
 Context* context_create(int device) { return new Context(device); }
@@ -634,5 +632,21 @@ double context_fp64_peak(Context* c, int reps) {
   return c->fp64_peak(reps);
 }
 int context_sm_count(const Context* c) { return c->sm_count(); }
+void context_set_kernels(Context* c, int br, int ks, int pack) {
+  CtxLock l(c->mu);
+  c->br_variant = br;
+  c->ks_variant = ks;
+  c->level_packing = pack;
+}
+void context_get_kernels(Context* c, int* br, int* ks, int* pack) {
+  CtxLock l(c->mu);
+  if (br) *br = c->br_variant;
+  if (ks) *ks = c->ks_variant;
+  if (pack) *pack = c->level_packing;
+}
+bool context_level_packing(Context* c) {
+  const int p = c->level_packing;
+  return p < 0 ? level_packing() : p != 0;
+}
 
 }  // namespace cvm

@@ -87,6 +87,10 @@ void context_event(Context* c, int which);
 double context_event_elapsed(Context* c);
 double context_fp64_peak(Context* c, int reps);
 int context_sm_count(const Context* c);
+// Per-context kernel choices (-1 = follow the process-wide setting).
+void context_set_kernels(Context* c, int br, int ks, int pack);
+void context_get_kernels(Context* c, int* br, int* ks, int* pack);
+bool context_level_packing(Context* c);
 
 // --------------------------------------------------------------- backend --
 // Mirror of cryptovm::Backend (gates.hpp:109-132) with handles as dense node

@@ -37,7 +37,8 @@ cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2,
 // bkf4 / tw4: the key in the warp-FFT bin order and the per-lane twiddle
 // bases of the v4 kernels (blind_rotate_v4.cu, fft512w.cuh).
 cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, cudaStream_t s);
-cudaError_t launch_blind_rotate(const BrJob* jobs, int count, const uint32_t* slab,
+// variant < 0: the process-wide setting (br_variant()).
+cudaError_t launch_blind_rotate(int variant, const BrJob* jobs, int count, const uint32_t* slab,
                                 const c64* bkf, const c64* tw1, const c64* tw2,
                                 const c64* bkf4, const c64* tw4, uint32_t* xout,
                                 cudaStream_t s);
@@ -46,26 +47,22 @@ bool valid_br_v4_variant(int v);
 cudaError_t launch_blind_rotate_v4(int variant, const BrJob* jobs, int count,
                                    const uint32_t* slab, const c64* bkf4, const c64* tw4,
                                    uint32_t* xout, cudaStream_t s);
-// Blind-rotation kernel variant: 1 = v1 (one bootstrap per 64-thread CTA, key
-// via L1); 10*G + S = v2 (G bootstraps per CTA, S-stage bulk-copy key ring:
-// 13, 22, 23, 43); 3044 = v3 (G=4, S=4, two transforms per thread);
-// 4044 = v3 with the key ring in tensor memory (tcgen05.cp / tcgen05.ld);
-// 5044 / 5054 / 5063 = v3 G=4 / v3 G=5 / v2 G=6 with generated twiddles
-// (TwPow8; 5044 is the wide-level default);
-// 6000 + 100*(1 - hold) + 10*G + S = v4 (one bootstrap per warp, warp-wide
-// FFT, G warps per CTA on an S-row key ring: 6184, 6185, 6084, 6085);
-// 9 = wide latency kernel.  0 = auto by level width (default).  Env
-// CVM_BR_KERNEL overrides the default.
+// Blind-rotation kernel variant (a pinned choice; every one is bit-identical):
+// 6000 + 10*W + 5 = v4 (one bootstrap per warp on the warp-wide FFT, W warps
+// per CTA on a 5-row key ring; 6085 = full waves); 5247 = v3 (four
+// bootstraps per CTA, 64-thread FFT, 7-row ring: wide-level remainders);
+// 9 = wide (one bootstrap per SM, the six rows transformed concurrently);
+// 96 = pair (one bootstrap per 2-SM cluster).  0 = auto by level width
+// (default).  Env CVM_BR_KERNEL overrides the default.
 constexpr int kDefaultBrVariant = 0;
 int br_variant();
 void set_br_variant(int v);
 bool valid_br_variant(int v);
-// Key-switch kernel: 1 = one gate per CTA; 6 = one gate per 948-thread CTA
-// (6 position groups, latency); 7 = the whole level as one INT8 tensor-core
-// product (one-hot digits x byte limbs of the KSK) on mma.sync; 8 = the same
-// product on tcgen05.mma with TMEM accumulators; 9 = 8 split along the
-// coefficients (K) into up to 16 CTAs per tile plus a reduction, so a narrow
-// level still fills the GPU; 0 = auto (9).  Env CVM_KS_KERNEL.
+// Key-switch kernel: the level as one INT8 tcgen05 product (one-hot digits x
+// byte limbs of the KSK, TMEM accumulators); 8 = one CTA per 128 x 128 tile,
+// 9 = the tiles split along the coefficients (K) into up to 16 CTAs plus a
+// reduction, so a narrow level still fills the GPU; 0 = auto (9).  Env
+// CVM_KS_KERNEL.
 constexpr int kDefaultKsVariant = 0;
 int ks_variant();
 void set_ks_variant(int v);
@@ -73,19 +70,17 @@ bool valid_ks_variant(int v);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t s);
 cudaError_t launch_gather_lwe(const uint32_t* slab, const uint64_t* slots, uint64_t count,
                               uint32_t* out, cudaStream_t s);
-// kskb: the KSK as byte limbs for variant 7 (see key_switch.cu), built by
-// launch_ksk_to_limbs from the padded [i][j][v][632] KSK.
-cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s);
-constexpr size_t kKskbWords = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
-// ksktc: the byte limbs pre-arranged as tcgen05 B tiles for variant 8
-// (1024 coefficients x 5 column tiles x 4 limbs x 4 KB).
+// ksktc: the KSK's byte limbs pre-arranged as tcgen05 B tiles (1024
+// coefficients x 5 column tiles x 4 limbs x 4 KB), built at key upload from
+// the padded [i][j][v][632] KSK (freed afterwards).
 cudaError_t launch_ksk_to_tc(const uint32_t* ksk, uint32_t* ksktc, cudaStream_t s);
 constexpr size_t kKskTcWords = size_t(kPolyN) * 5 * 4 * 1024;
 // kspart: split-K scratch of variant 9, kKsPartWords u32.
 constexpr int kKsMaxSplits = 16;
 constexpr size_t kKsPartWords = size_t(148 / 5) * 128 * 640;
-cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
-                              const uint32_t* ksk, const uint32_t* kskb, const uint32_t* ksktc,
-                              uint32_t* kspart, uint32_t* slab, cudaStream_t s);
+// variant < 0: the process-wide setting (ks_variant()).
+cudaError_t launch_key_switch(int variant, const KsJob* jobs, int count, const uint32_t* xlwe,
+                              const uint32_t* ksktc, uint32_t* kspart, uint32_t* slab,
+                              cudaStream_t s);
 
 }  // namespace cvm

@@ -1,11 +1,16 @@
-// sm_100a key-switch kernels (K3 + K4: MUX combine, LWE key switch
-// N = 1024 -> n = 630):
-//   key_switch_kernel       one gate per CTA (160 threads);
-//   key_switch_wide_kernel  one gate per CTA, 6 position groups (narrow levels);
-//   key_switch_mma_kernel   a level as one INT8 product on mma.sync;
-//   key_switch_tc_kernel    the same product on tcgen05.mma with the limb
-//                           accumulators in tensor memory (wide-level default).
-// Bit-identical; DESIGN.md section 4.4.
+// sm_100a key switch (K3 + K4: MUX combine, LWE key switch N = 1024 ->
+// n = 630) of a whole level as one integer matrix product on the tcgen05
+// tensor cores:
+//   out[g][col] = b_g - sum_{i,j} KSK[i][j][d_gij][col]
+//              = b_g - (A x B)[g][col],  A[g][(i,j,v)] = [d_gij == v] (one-hot),
+// B[(i,j,v)][col] = KSK[i][j][v][col].  B's 32-bit torus words are split into
+// four byte limbs, each product exact in u8 x u8 -> s32 (a column sum is at
+// most 8192 * 255 < 2^31), recombined mod 2^32 as sum_l acc_l << 8 l.
+// K = 1024 coefficients x 8 digits x 4 values, one coefficient per k32 step.
+// Variant 8: one CTA per 128-gate x 128-column tile; variant 9 (default):
+// the same tiles split along K over up to 16 CTAs + ks_reduce_kernel.
+// (Round 1's gather kernels and the mma.sync product are retired; their
+// numbers are in profiles/r01_variant_sweep.txt.)  DESIGN.md section 4.4.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -18,294 +23,8 @@
 
 namespace cvm {
 
-// ------------------------------------------------------------ K3 + K4 --
-// One key switch per CTA; thread t owns output columns 4t..4t+3 (uint4).
-__global__ void __launch_bounds__(kKsThreads) key_switch_kernel(
-    const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
-    const uint4* __restrict__ ksk, uint32_t* __restrict__ slab) {
-  constexpr int kRowVec = kKskRowStride / 4;  // 158 uint4 per row
-  __shared__ uint32_t x[kXlweWords];
-  const int t = threadIdx.x;
-  const KsJob job = jobs[blockIdx.x];
-  for (int i = t; i < kXlweWords; i += kKsThreads) {
-    uint32_t v = xlwe[(size_t)job.x[0] * kXlweStride + i];
-    if (job.x[1] != kNoInput) v += xlwe[(size_t)job.x[1] * kXlweStride + i];
-    if (i == kPolyN) v += job.cst;
-    x[i] = v;
-  }
-  __syncthreads();
-  if (t >= kRowVec) return;
-  uint4 a = {0u, 0u, 0u, 0u};
-  if (t == kN / 4) a.z = x[kPolyN];  // column 630 holds b
-  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
-#pragma unroll 2
-  for (int i = 0; i < kPolyN; ++i) {
-    const uint32_t abar = x[i] + prec;
-    const uint4* base = ksk + (size_t)i * (kKsT * kKsBase * kRowVec) + t;
-#pragma unroll
-    for (int j = 0; j < kKsT; ++j) {
-      const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
-      if (d == 0) continue;  // the d = 0 rows are zero (uniform across the CTA)
-      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);
-      a.x -= r.x;
-      a.y -= r.y;
-      a.z -= r.z;
-      a.w -= r.w;
-    }
-  }
-  reinterpret_cast<uint4*>(slab + (size_t)job.out_slot * kLweStride)[t] = a;
-}
-
-// Latency variant: 6 position groups of 158 threads gather concurrently and
-// are reduced through shared memory -- ~6x shorter dependent load chain.
-constexpr int kKsWidePG = 6;
-constexpr int kKsWideThreads = kKsWidePG * (kKskRowStride / 4);  // 948
-
-__global__ void __launch_bounds__(kKsWideThreads) key_switch_wide_kernel(
-    const KsJob* __restrict__ jobs, const uint32_t* __restrict__ xlwe,
-    const uint4* __restrict__ ksk, uint32_t* __restrict__ slab) {
-  constexpr int kRowVec = kKskRowStride / 4;
-  __shared__ uint32_t x[kXlweWords];
-  __shared__ uint4 part[kKsWidePG - 1][kRowVec];
-  const int tid = threadIdx.x;
-  const int col = tid % kRowVec, pg = tid / kRowVec;
-  const KsJob job = jobs[blockIdx.x];
-  for (int i = tid; i < kXlweWords; i += kKsWideThreads) {
-    uint32_t v = xlwe[(size_t)job.x[0] * kXlweStride + i];
-    if (job.x[1] != kNoInput) v += xlwe[(size_t)job.x[1] * kXlweStride + i];
-    if (i == kPolyN) v += job.cst;
-    x[i] = v;
-  }
-  __syncthreads();
-  uint4 a = {0u, 0u, 0u, 0u};
-  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
-  const int i0 = pg * kPolyN / kKsWidePG, i1 = (pg + 1) * kPolyN / kKsWidePG;
-#pragma unroll 2
-  for (int i = i0; i < i1; ++i) {
-    const uint32_t abar = x[i] + prec;
-    const uint4* base = ksk + (size_t)i * (kKsT * kKsBase * kRowVec) + col;
-#pragma unroll
-    for (int j = 0; j < kKsT; ++j) {
-      const uint32_t d = (abar >> (32 - (j + 1) * kKsBaseBit)) & (kKsBase - 1);
-      if (d == 0) continue;
-      const uint4 r = __ldg(base + (j * kKsBase + d) * kRowVec);
-      a.x -= r.x;
-      a.y -= r.y;
-      a.z -= r.z;
-      a.w -= r.w;
-    }
-  }
-  if (pg > 0) part[pg - 1][col] = a;
-  __syncthreads();
-  if (pg == 0) {
-#pragma unroll
-    for (int k = 0; k < kKsWidePG - 1; ++k) {
-      const uint4 r = part[k][col];
-      a.x += r.x;
-      a.y += r.y;
-      a.z += r.z;
-      a.w += r.w;
-    }
-    if (col == kN / 4) a.z += x[kPolyN];  // column 630 holds b
-    reinterpret_cast<uint4*>(slab + (size_t)job.out_slot * kLweStride)[col] = a;
-  }
-}
-
-// ------------------------------------------- K3 + K4 on the tensor cores --
-// The key switch of a whole level as one integer matrix product:
-//   out[g][col] = b_g - sum_{i,j} KSK[i][j][d_gij][col]
-//              = b_g - (A x B)[g][col],  A[g][(i,j,v)] = [d_gij == v] (one-hot),
-// B[(i,j,v)][col] = KSK[i][j][v][col].  B's 32-bit torus words are split into
-// four byte limbs, each multiplied exactly on the INT8 tensor cores (mma.sync
-// m16n8k32 u8 x u8 -> s32: a column sum is at most 8192 * 255 < 2^31) and
-// recombined mod 2^32 as sum_l acc_l << 8l -- bit-identical to the gathers.
-// K = 1024 coefficients x 8 digits x 4 values (the v = 0 rows are zero), one
-// coefficient per k32 step: A's byte k = 4j + v of a step is the one-hot of
-// digit j, so a thread's A register is just 1 << 8*digit.
-//
-// CTA tile: 128 gates x 48 columns x 4 limbs; 8 warps = 4 gate groups (32
-// gates = 2 m16 tiles) x 2 column groups (24 columns = 3 n8 tiles); every B
-// fragment feeds both m tiles.  B chunks (4 coefficients, 48 KB... 57 KB with
-// padding) and the gates' digit words stream through a 2-stage cp.async ring.
-//
-// B layout in HBM (kskb, built once per key upload by ksk_to_limbs_kernel):
-//   [i 1024][limb 4][j 8][col 632] u32 = bytes v = 0..3 of limb l of
-//   KSK[i][j][v][col]   (82.8 MB).
-constexpr int kKsmGates = 128;
-constexpr int kKsmCols = 48;
-constexpr int kKsmColTiles = (kKskRowStride + kKsmCols - 1) / kKsmCols;  // 14
-constexpr int kKsmChunk = 4;                                             // coefficients / stage
-constexpr int kKsmBStride = 56;  // padded column stride: conflict-free fragment loads
-constexpr int kKsmThreads = 256;
-
-struct KsmSmem {
-  uint32_t b[2][kKsmChunk][4][8][kKsmBStride];
-  uint32_t abar[2][kKsmChunk][kKsmGates];
-  KsJob job[kKsmGates];
-  uint32_t bval[kKsmGates];
-};
-
-__global__ void __launch_bounds__(256) ksk_to_limbs_kernel(const uint32_t* __restrict__ ksk,
-                                                           uint32_t* __restrict__ kskb) {
-  // one thread per (i, l, j, col) output word
-  const size_t idx = size_t(blockIdx.x) * 256 + threadIdx.x;
-  const size_t total = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
-  if (idx >= total) return;
-  const int col = int(idx % kKskRowStride);
-  const int j = int((idx / kKskRowStride) % kKsT);
-  const int l = int((idx / (size_t(kKskRowStride) * kKsT)) % 4);
-  const int i = int(idx / (size_t(kKskRowStride) * kKsT * 4));
-  uint32_t w = 0;
-#pragma unroll
-  for (int v = 0; v < kKsBase; ++v) {
-    const uint32_t x = ksk[((size_t(i) * kKsT + j) * kKsBase + v) * kKskRowStride + col];
-    w |= ((x >> (8 * l)) & 0xFFu) << (8 * v);
-  }
-  kskb[idx] = w;
-}
-
-__device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                       uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__global__ void __launch_bounds__(kKsmThreads) key_switch_mma_kernel(
-    const KsJob* __restrict__ jobs, int count, const uint32_t* __restrict__ xlwe,
-    const uint32_t* __restrict__ kskb, uint32_t* __restrict__ slab) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  KsmSmem& sm = *reinterpret_cast<KsmSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g0 = blockIdx.x * kKsmGates;
-  const int c0 = blockIdx.y * kKsmCols;
-  const uint32_t prec = 1u << (32 - (1 + kKsBaseBit * kKsT));
-
-  if (tid < kKsmGates) {
-    const int g = g0 + tid;
-    KsJob jb = jobs[g < count ? g : 0];
-    sm.job[tid] = jb;
-    uint32_t b = xlwe[size_t(jb.x[0]) * kXlweStride + kPolyN] + jb.cst;
-    if (jb.x[1] != kNoInput) b += xlwe[size_t(jb.x[1]) * kXlweStride + kPolyN];
-    sm.bval[tid] = b;
-  }
-  __syncthreads();
-
-  // stage loaders: B rows (i, l, j) of 48 columns as 12 x 16 B; digit words
-  // abar[i][g] = x0 + x1 + prec for the chunk's 4 coefficients (one uint4 per
-  // gate and input)
-  auto load_b = [&](int stage, int chunk) {
-    for (int e = tid; e < kKsmChunk * 4 * 8 * 12; e += kKsmThreads) {
-      const int seg = e % 12, row = e / 12;  // row = (ii*4 + l)*8 + j
-      const int col = c0 + seg * 4;
-      if (col >= kKskRowStride) continue;
-      const int ii = row / 32, lj = row % 32;
-      const uint32_t* src = kskb + (size_t(chunk * kKsmChunk + ii) * 32 + lj) * kKskRowStride + col;
-      cp_async16(&sm.b[stage][ii][lj >> 3][lj & 7][seg * 4], src);
-    }
-  };
-  auto load_abar = [&](int chunk, uint4& v) {
-    if (tid < kKsmGates) {
-      const KsJob& jb = sm.job[tid];
-      v = *reinterpret_cast<const uint4*>(xlwe + size_t(jb.x[0]) * kXlweStride +
-                                          chunk * kKsmChunk);
-      if (jb.x[1] != kNoInput) {
-        const uint4 w = *reinterpret_cast<const uint4*>(
-            xlwe + size_t(jb.x[1]) * kXlweStride + chunk * kKsmChunk);
-        v.x += w.x;
-        v.y += w.y;
-        v.z += w.z;
-        v.w += w.w;
-      }
-    }
-  };
-  auto store_abar = [&](int stage, const uint4& v) {
-    if (tid < kKsmGates) {
-      sm.abar[stage][0][tid] = v.x + prec;
-      sm.abar[stage][1][tid] = v.y + prec;
-      sm.abar[stage][2][tid] = v.z + prec;
-      sm.abar[stage][3][tid] = v.w + prec;
-    }
-  };
-
-  const int wg = warp & 3, wc = warp >> 2;
-  const int grp = lane >> 2, tig = lane & 3;
-  int acc[2][3][4][4];
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-      for (int l = 0; l < 4; ++l)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[mt][nt][l][r] = 0;
-
-  constexpr int kChunks = kPolyN / kKsmChunk;  // 256
-  uint4 xv = {0, 0, 0, 0};
-  load_b(0, 0);
-  cp_async_commit();
-  load_abar(0, xv);
-  store_abar(0, xv);
-  for (int c = 0; c < kChunks; ++c) {
-    const int st = c & 1;
-    cp_async_wait_all();
-    __syncthreads();  // chunk c resident; everyone is done with stage st ^ 1
-    if (c + 1 < kChunks) {
-      load_b(st ^ 1, c + 1);
-      cp_async_commit();
-      load_abar(c + 1, xv);
-    }
-#pragma unroll
-    for (int ii = 0; ii < kKsmChunk; ++ii) {
-      uint32_t a[2][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int gl = wg * 32 + mt * 16 + grp;
-        const uint32_t lo = sm.abar[st][ii][gl], hi = sm.abar[st][ii][gl + 8];
-        const int s0 = 30 - 2 * tig, s1 = 22 - 2 * tig;  // digits tig and tig + 4
-        a[mt][0] = 1u << (8 * ((lo >> s0) & 3u));
-        a[mt][1] = 1u << (8 * ((hi >> s0) & 3u));
-        a[mt][2] = 1u << (8 * ((lo >> s1) & 3u));
-        a[mt][3] = 1u << (8 * ((hi >> s1) & 3u));
-      }
-#pragma unroll
-      for (int nt = 0; nt < 3; ++nt) {
-        const int col = wc * 24 + nt * 8 + grp;
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const uint32_t b0 = sm.b[st][ii][l][tig][col];
-          const uint32_t b1 = sm.b[st][ii][l][tig + 4][col];
-          mma_u8(acc[0][nt][l], a[0], b0, b1);
-          mma_u8(acc[1][nt][l], a[1], b0, b1);
-        }
-      }
-    }
-    if (c + 1 < kChunks) store_abar(st ^ 1, xv);
-  }
-
-  // epilogue: recombine the limbs, subtract from b (column 630), write
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int gl = wg * 32 + mt * 16 + grp + (r >= 2 ? 8 : 0);
-        const int col = c0 + wc * 24 + nt * 8 + tig * 2 + (r & 1);
-        if (g0 + gl >= count || col >= kKskRowStride) continue;
-        const uint32_t sum = uint32_t(acc[mt][nt][0][r]) + (uint32_t(acc[mt][nt][1][r]) << 8) +
-                             (uint32_t(acc[mt][nt][2][r]) << 16) +
-                             (uint32_t(acc[mt][nt][3][r]) << 24);
-        const uint32_t base = col == kN ? sm.bval[gl] : 0u;
-        slab[size_t(sm.job[gl].out_slot) * kLweStride + col] = base - sum;
-      }
-}
-
 // ------------------------------- K3 + K4 on tcgen05 (5th-gen tensor cores) --
-// The same one-hot x byte-limb product as key_switch_mma_kernel, issued as
-// tcgen05.mma kind::i8 (u8 x u8 -> s32) with the four limb accumulators in
+// The one-hot x byte-limb product issued as tcgen05.mma kind::i8 (u8 x u8 -> s32) with the four limb accumulators in
 // tensor memory: CTA tile 128 gates (M) x 128 columns (N) x 4 limbs = all 512
 // TMEM columns; one k32 step per coefficient (4 MMAs, one per limb).
 //   warps 0-3 (128 threads, thread = gate = TMEM lane): write the one-hot A
@@ -550,44 +269,23 @@ int ks_variant() {
   return g_ks_variant;
 }
 void set_ks_variant(int v) { g_ks_variant = v; }
-bool valid_ks_variant(int v) { return v == 0 || v == 1 || v == 6 || v == 7 || v == 8 || v == 9; }
-
-cudaError_t launch_ksk_to_limbs(const uint32_t* ksk, uint32_t* kskb, cudaStream_t s) {
-  const size_t total = size_t(kPolyN) * 4 * kKsT * kKskRowStride;
-  ksk_to_limbs_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(ksk, kskb);
-  return cudaGetLastError();
-}
+bool valid_ks_variant(int v) { return v == 0 || v == 8 || v == 9; }
 
 cudaError_t launch_ksk_to_tc(const uint32_t* ksk, uint32_t* ksktc, cudaStream_t s) {
   ksk_to_tc_kernel<<<unsigned((kKskTcWords + 255) / 256), 256, 0, s>>>(ksk, ksktc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_key_switch(const KsJob* jobs, int count, const uint32_t* xlwe,
-                              const uint32_t* ksk, const uint32_t* kskb, const uint32_t* ksktc,
-                              uint32_t* kspart, uint32_t* slab, cudaStream_t s) {
+cudaError_t launch_key_switch(int variant, const KsJob* jobs, int count, const uint32_t* xlwe,
+                              const uint32_t* ksktc, uint32_t* kspart, uint32_t* slab,
+                              cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  const uint4* k4 = reinterpret_cast<const uint4*>(ksk);
-  int variant = ks_variant();
+  if (variant < 0) variant = ks_variant();
   // auto: the split-K tcgen05 product at every width (0.037 ms for a
   // 32-gate level vs 0.178 for the 6-group gather and 0.26 unsplit; equal to
   // the unsplit product on wide levels; profiles/r01_variant_sweep.txt)
   if (variant == 0) variant = 9;
   switch (variant) {
-    case 1: key_switch_kernel<<<count, kKsThreads, 0, s>>>(jobs, xlwe, k4, slab); break;
-    case 6:
-      key_switch_wide_kernel<<<count, kKsWideThreads, 0, s>>>(jobs, xlwe, k4, slab);
-      break;
-    case 7: {
-      if (!kskb) return cudaErrorInvalidValue;
-      static std::atomic<uint64_t> configured{0};
-      const int smem = int(sizeof(KsmSmem));
-      cudaError_t e = set_smem(key_switch_mma_kernel, smem, configured);
-      if (e != cudaSuccess) return e;
-      const dim3 grid((count + kKsmGates - 1) / kKsmGates, kKsmColTiles);
-      key_switch_mma_kernel<<<grid, kKsmThreads, smem, s>>>(jobs, count, xlwe, kskb, slab);
-      break;
-    }
     case 8: {
       if (!ksktc) return cudaErrorInvalidValue;
       static std::atomic<uint64_t> configured{0};

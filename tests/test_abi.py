@@ -71,18 +71,20 @@ def test_process_wide_kernel_knobs():
     lib = N.lib
     br, ks, pack = lib.cvm_get_br_variant(), lib.cvm_get_ks_variant(), lib.cvm_get_level_packing()
     try:
-        for v in (0, 1, 9, 13, 92, 96, 5247, 6085, 6185, 6015, 6084):
+        for v in (0, 9, 96, 5247, 6085, 6015, 6045):
             N.check(lib.cvm_set_br_variant(v))
             assert lib.cvm_get_br_variant() == v
-        for v in (2, 7000, 6095, 6086, 6485):
+        # retired round-1 variants and malformed numbers are rejected
+        for v in (1, 13, 92, 4044, 5044, 6185, 6084, 6095, 6005, 7000):
             with pytest.raises(P.CvmInputError):
                 N.check(lib.cvm_set_br_variant(v))
-            assert lib.cvm_get_br_variant() == 6084
-        for v in (0, 1, 6, 7, 8, 9):
+            assert lib.cvm_get_br_variant() == 6045
+        for v in (0, 8, 9):
             N.check(lib.cvm_set_ks_variant(v))
             assert lib.cvm_get_ks_variant() == v
-        with pytest.raises(P.CvmInputError):
-            N.check(lib.cvm_set_ks_variant(5))
+        for v in (1, 5, 6, 7):
+            with pytest.raises(P.CvmInputError):
+                N.check(lib.cvm_set_ks_variant(v))
         for v in (0, 1):
             N.check(lib.cvm_set_level_packing(v))
             assert lib.cvm_get_level_packing() == v

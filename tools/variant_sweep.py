@@ -13,7 +13,7 @@ from paper_2101_03403_b200._native import check, lib  # noqa: E402
 
 def main():
     n = int(os.environ.get("N_NAND", 4096))
-    variants = [int(v) for v in os.environ.get("VARIANTS", "1,13,22,23,43").split(",")]
+    variants = [int(v) for v in os.environ.get("VARIANTS", "6085,5247,9,96").split(",")]
     ks = P.KeySet(1)
     ctx = P.Context(0)
     ctx.upload_keyset(ks)
@@ -44,7 +44,7 @@ def main():
                   "decrypt_ok": ok}
         print(v, res[v], flush=True)
     check(lib.cvm_set_br_variant(0))
-    for kv in [int(v) for v in os.environ.get("KS_VARIANTS", "1,4,8").split(",")]:
+    for kv in [int(v) for v in os.environ.get("KS_VARIANTS", "8,9").split(",")]:
         check(lib.cvm_set_ks_variant(kv))
         best = None
         for _ in range(3):
