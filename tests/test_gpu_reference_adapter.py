@@ -32,3 +32,36 @@ def test_ciphertext_image_on_reference_sim_backend():
     r = subprocess.run([CT_CHECK], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "CT IMAGE OK" in r.stdout
+
+
+RUN = os.path.join(REPO, "integration", "_build", "cryptovm_run")
+LOOP = """.word_size 16
+MOV R0 0
+MOV R1 13
+MOV R2 11
+again:
+ADD R0 R0 R1
+SUBS R2 R2 1
+B_NE again
+HALT
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(RUN), reason="cryptovm_run not built (needs /root/reference)")
+def test_cli_run_backend_gpu(tmp_path):
+    """SURVEY f-4: the reference CLI's `run` flow with --backend gpu (the
+    Machine on cryptovm::GpuBackend) gives the SimBackend's registers, branch
+    count and schedule report."""
+    import json
+    prog = tmp_path / "loop.s"
+    prog.write_text(LOOP)
+    out = {}
+    for kind in ("sim", "gpu"):
+        r = subprocess.run([RUN, str(prog), "--backend", kind, "--regs", "4"],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        out[kind] = json.loads(r.stdout)
+    assert out["gpu"]["registers"] == [143, 13, 0, 0] == out["sim"]["registers"]
+    assert out["gpu"]["branch_queries"] == out["sim"]["branch_queries"] == 11
+    assert out["gpu"]["schedule"] == out["sim"]["schedule"]
