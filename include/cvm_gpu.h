@@ -250,6 +250,17 @@ typedef struct cvm_backend_stats {
   uint64_t executed, executed_bootstraps, pending;
 } cvm_backend_stats;
 CVM_API int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out);
+/* Region attribution (the reference's GateDag region labels, dag.hpp:55-70):
+ * push_region / pop_region build a path ("adder/carry/level1"); every gate
+ * records the path open at its recording.  Region 0 is "" (outside any
+ * region).  recorded = bootstrapped gates recorded in the region, executed =
+ * those evaluated so far (dead gates never are).  Flushes also emit NVTX
+ * ranges per launch labelled with these regions (when a profiler is attached
+ * or CVM_NVTX=1). */
+CVM_API int cvm_backend_region_count(const cvm_backend* b, uint64_t* out);
+CVM_API int cvm_backend_region_info(const cvm_backend* b, uint64_t idx, char* name,
+                                    size_t name_size, uint64_t* recorded,
+                                    uint64_t* executed);
 /* Node table: kind, input flag, deps (0 = none), constant value per node id. */
 CVM_API int cvm_backend_node_count(const cvm_backend* b, uint64_t* out);
 CVM_API int cvm_backend_nodes(const cvm_backend* b, uint64_t first, uint64_t count,
@@ -283,8 +294,9 @@ typedef struct cvm_dag_node {
 CVM_API int cvm_backend_replay_dag(cvm_backend* b, const cvm_dag_node* nodes,
                                    uint64_t n_nodes, const cvm_handle* inputs,
                                    uint64_t n_inputs, cvm_handle* handles);
-/* Evaluate the cone of influence of `count` handles now (one flush), so the
- * key owner's later bit-by-bit decryptions (word.cpp:70-77) only download. */
+/* Evaluate the cone of influence of `count` handles now (one flush) and
+ * download their values once into a host cache, so the key owner's later
+ * bit-by-bit decryptions (word.cpp:70-77) need no device round trip each. */
 CVM_API int cvm_backend_evaluate(cvm_backend* b, size_t count, const cvm_handle* hs);
 
 /* `batch` independent instances of one recorded circuit through the public

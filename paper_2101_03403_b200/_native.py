@@ -131,6 +131,8 @@ _SIGS = {
     "cvm_backend_flush": (_i, [_p]),
     "cvm_backend_set_flush_policy": (_i, [_p, _i]),
     "cvm_backend_stats_get":(_i, [_p, ctypes.POINTER(BackendStats)]),
+    "cvm_backend_region_count": (_i, [_p, _u64p]),
+    "cvm_backend_region_info": (_i, [_p, _u64, ctypes.c_char_p, ctypes.c_size_t, _u64p, _u64p]),
     "cvm_backend_node_count": (_i, [_p, _u64p]),
     "cvm_backend_nodes": (_i, [_p, _u64, _u64, _p]),
     "cvm_backend_capture_plan": (_i, [_p, ctypes.POINTER(_p)]),

@@ -339,6 +339,19 @@ class Backend:
         check(lib.cvm_backend_stats_get(self._h, ctypes.byref(s)))
         return s.as_dict()
 
+    def regions(self):
+        """{region path: (recorded bootstrapped gates, executed)}."""
+        n = ctypes.c_uint64()
+        check(lib.cvm_backend_region_count(self._h, ctypes.byref(n)))
+        out = {}
+        buf = ctypes.create_string_buffer(512)
+        rec, exe = ctypes.c_uint64(), ctypes.c_uint64()
+        for i in range(n.value):
+            check(lib.cvm_backend_region_info(self._h, i, buf, len(buf), ctypes.byref(rec),
+                                              ctypes.byref(exe)))
+            out[buf.value.decode()] = (rec.value, exe.value)
+        return out
+
     def nodes(self):
         n = ctypes.c_uint64()
         check(lib.cvm_backend_node_count(self._h, ctypes.byref(n)))

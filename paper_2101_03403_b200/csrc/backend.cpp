@@ -27,6 +27,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cvm_internal.hpp"
 
 namespace cvm {
@@ -74,6 +76,8 @@ cvm_operand GpuBackend::operand(Bit h) const {
 
 Bit GpuBackend::record_gate(Node n, const cvm_gate& g) {
   n.gate_idx = uint32_t(gates_.size());
+  n.region = region_stack_.empty() ? 0u : region_stack_.back();
+  region_recorded_[n.region]++;
   gates_.push_back(g);
   const Bit id = add_node(n);
   pending_.push_back(id);
@@ -225,6 +229,8 @@ bool GpuBackend::release_slots() {
   if (!context_release_slots(ctx_, r.front().first, r.back().second)) return false;
   runs_.clear();
   next_slot_ = chunk_end_ = 0;
+  cache_.clear();
+  slot_evaluated_.clear();
   return true;
 }
 
@@ -264,19 +270,25 @@ void set_level_packing(bool on) { g_pack.store(on ? 1 : 0); }
 // Groups the selected pending gates into launches (their pending inputs are
 // selected too, so levels stay consistent): by dataflow level, or -- the
 // default -- wave-packed (pack_levels).
-std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(const std::vector<Bit>& ids) const {
+std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(
+    const std::vector<Bit>& ids, std::vector<std::vector<Bit>>* ids_out) const {
   uint32_t depth = 0;
   for (Bit id : ids) depth = std::max(depth, nodes_[id - 1].level);
   if (context_level_packing(ctx_) && depth > 1 && ids.size() > size_t(kPackMinGates))
-    return pack_levels(ids, depth);
+    return pack_levels(ids, depth, ids_out);
   std::vector<std::vector<cvm_gate>> lv;
+  std::vector<std::vector<Bit>> li;
   for (Bit id : ids) {
     const Node& n = nodes_[id - 1];
-    if (lv.size() < n.level) lv.resize(n.level);
+    if (lv.size() < n.level) lv.resize(n.level), li.resize(n.level);
     lv[n.level - 1].push_back(gates_[n.gate_idx]);
+    li[n.level - 1].push_back(id);
   }
   lv.erase(std::remove_if(lv.begin(), lv.end(), [](const auto& v) { return v.empty(); }),
            lv.end());
+  li.erase(std::remove_if(li.begin(), li.end(), [](const auto& v) { return v.empty(); }),
+           li.end());
+  if (ids_out) *ids_out = std::move(li);
   return lv;
 }
 
@@ -288,8 +300,8 @@ std::vector<std::vector<cvm_gate>> GpuBackend::levels_of(const std::vector<Bit>&
 // 8192, 7680, 7424, 6656 (each with a partial wave).  Gates are pure, so
 // results are unchanged (tests/test_gpu_parity.py compares packed and plain
 // runs; tests/native/schedule_test.cpp checks the schedule's invariants).
-std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(std::vector<Bit> ids,
-                                                           uint32_t depth) const {
+std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(
+    std::vector<Bit> ids, uint32_t depth, std::vector<std::vector<Bit>>* ids_out) const {
   std::sort(ids.begin(), ids.end());  // node ids are a topological order
   const size_t G = ids.size();
   const Bit lo = ids.front(), hi = ids.back();
@@ -318,9 +330,16 @@ std::vector<std::vector<cvm_gate>> GpuBackend::pack_levels(std::vector<Bit> ids,
   }
   const std::vector<uint32_t> launch = pack_schedule(pred, boots);
   std::vector<std::vector<cvm_gate>> out(depth);
-  for (size_t i = 0; i < G; ++i) out[launch[i] - 1].push_back(gates_[nodes_[ids[i] - 1].gate_idx]);
+  std::vector<std::vector<Bit>> li(depth);
+  for (size_t i = 0; i < G; ++i) {
+    out[launch[i] - 1].push_back(gates_[nodes_[ids[i] - 1].gate_idx]);
+    li[launch[i] - 1].push_back(ids[i]);
+  }
   out.erase(std::remove_if(out.begin(), out.end(), [](const auto& v) { return v.empty(); }),
             out.end());
+  li.erase(std::remove_if(li.begin(), li.end(), [](const auto& v) { return v.empty(); }),
+           li.end());
+  if (ids_out) *ids_out = std::move(li);
   return out;
 }
 
@@ -353,15 +372,37 @@ void GpuBackend::retire(const std::vector<Bit>& done) {
 void GpuBackend::run(const std::vector<Bit>& ids) {
   context_reserve(ctx_, context_slots_used(ctx_));
   stage_uploads();
-  const auto lv = levels_of(ids);
+  std::vector<std::vector<Bit>> lids;
+  const auto lv = levels_of(ids, &lids);
+  for (Bit id : ids) {
+    const Node& n = nodes_[id - 1];
+    region_executed_[n.region]++;
+    if (slot_evaluated_.empty()) slot_base_ = uint64_t(n.slot);
+    if (uint64_t(n.slot) < slot_base_) {
+      slot_evaluated_.insert(slot_evaluated_.begin(), slot_base_ - uint64_t(n.slot), 0);
+      slot_base_ = uint64_t(n.slot);
+    }
+    const uint64_t k = uint64_t(n.slot) - slot_base_;
+    if (k >= slot_evaluated_.size()) slot_evaluated_.resize(k + 1, 0);
+    slot_evaluated_[k] = 1;
+  }
+  // NVTX ranges per launch (nsys / ncu timelines), labelled with the
+  // regions of its gates; built only when a tool is attached or CVM_NVTX=1
+  static const bool nvtx = getenv("CUDA_INJECTION64_PATH") || getenv("CVM_NVTX");
+  if (nvtx) nvtxRangePushA(("cvm flush: " + std::to_string(ids.size()) + " gates, " +
+                            std::to_string(lv.size()) + " launches").c_str());
   uint64_t gates = 0, boots = 0;
-  for (const auto& level : lv) {
+  for (size_t k = 0; k < lv.size(); ++k) {
+    const auto& level = lv[k];
+    if (nvtx) nvtxRangePushA(level_label(k, lv.size(), lids[k]).c_str());
     context_submit_level(ctx_, level.data(), level.size());
+    if (nvtx) nvtxRangePop();
     gates += level.size();
     for (const auto& g : level) boots += g.kind == uint32_t(GateKind::Mux) ? 2 : 1;
     stats_.max_level_width = std::max<uint64_t>(stats_.max_level_width, level.size());
   }
   context_sync(ctx_);
+  if (nvtx) nvtxRangePop();
   stats_.flushes++;
   stats_.levels_run += lv.size();
   stats_.last_flush_levels = lv.size();
@@ -442,7 +483,7 @@ Plan* GpuBackend::capture_plan() {
   context_reserve(ctx_, context_slots_used(ctx_));
   stage_uploads();
   const std::vector<Bit> all = pending_;
-  const auto lv = levels_of(all);
+  const auto lv = levels_of(all, nullptr);
   Plan* p = context_make_plan(ctx_, lv);
   p->ran = std::make_shared<std::atomic<bool>>(all.empty());
   plans_.push_back(p->ran);
@@ -455,9 +496,50 @@ Plan* GpuBackend::capture_plan() {
   return p;
 }
 
+void GpuBackend::evaluate(size_t count, const Bit* hs) {
+  std::lock_guard<std::mutex> lock(mu_);
+  for (size_t i = 0; i < count; ++i) node(hs[i], "evaluate");
+  flush_for_locked(count, hs);
+  std::vector<uint64_t> sl;
+  for (size_t i = 0; i < count; ++i) {
+    const int64_t slot = nodes_[hs[i] - 1].slot;
+    if (slot < 0 || uint64_t(slot) < slot_base_) continue;
+    const uint64_t k = uint64_t(slot) - slot_base_;
+    if (k < slot_evaluated_.size() && slot_evaluated_[k] == 1) {
+      slot_evaluated_[k] = 2;  // queued / cached
+      sl.push_back(uint64_t(slot));
+    }
+  }
+  if (sl.empty()) return;
+  std::vector<uint32_t> buf(sl.size() * kLweWords);
+  context_gather_download(ctx_, sl.data(), sl.size(), buf.data());
+  for (size_t q = 0; q < sl.size(); ++q)
+    cache_[int64_t(sl[q])].assign(buf.begin() + q * kLweWords, buf.begin() + (q + 1) * kLweWords);
+}
+
 void GpuBackend::export_lwe(size_t count, const Bit* hs, uint32_t* out) {
   std::lock_guard<std::mutex> lock(mu_);
   for (size_t i = 0; i < count; ++i) node(hs[i], "export");
+  // served from the host cache when every requested value is there
+  bool cached = !cache_.empty();
+  for (size_t i = 0; i < count && cached; ++i) {
+    const Node& n = nodes_[hs[i] - 1];
+    cached = n.slot < 0 || (n.level == 0 && cache_.count(n.slot));
+  }
+  if (cached) {
+    for (size_t q = 0; q < count; ++q) {
+      const Node& n = nodes_[hs[q] - 1];
+      uint32_t* o = out + q * kLweWords;
+      if (n.slot < 0) {
+        std::memset(o, 0, kLweWords * 4);
+      } else {
+        const uint32_t* src = cache_.at(n.slot).data();
+        for (int w = 0; w < kLweWords; ++w) o[w] = n.sign > 0 ? src[w] : 0u - src[w];
+      }
+      o[kN] += n.constant;
+    }
+    return;
+  }
   if (cone_only_) {
     flush_for_locked(count, hs);
   } else {
@@ -510,13 +592,55 @@ void GpuBackend::decrypt_bits(size_t count, const Bit* hs, uint8_t* out) {
 
 void GpuBackend::push_region(std::string_view name) {
   std::lock_guard<std::mutex> lock(mu_);
-  regions_.emplace_back(name);
+  std::string path = region_stack_.empty() ? std::string(name)
+                                           : region_names_[region_stack_.back()] + "/" +
+                                                 std::string(name);
+  uint32_t idx = 0;
+  for (size_t i = 1; i < region_names_.size() && !idx; ++i)
+    if (region_names_[i] == path) idx = uint32_t(i);
+  if (!idx) {
+    idx = uint32_t(region_names_.size());
+    region_names_.push_back(std::move(path));
+    region_recorded_.push_back(0);
+    region_executed_.push_back(0);
+  }
+  region_stack_.push_back(idx);
 }
 
 void GpuBackend::pop_region() {
   std::lock_guard<std::mutex> lock(mu_);
-  if (regions_.empty()) throw InputError("pop_region without a matching push_region");
-  regions_.pop_back();
+  if (region_stack_.empty()) throw InputError("pop_region without a matching push_region");
+  region_stack_.pop_back();
+}
+
+size_t GpuBackend::region_count() const { return region_names_.size(); }
+void GpuBackend::region_info(size_t idx, std::string* name, uint64_t* recorded,
+                             uint64_t* executed) const {
+  if (idx >= region_names_.size()) throw InputError("region index out of range");
+  if (name) *name = region_names_[idx];
+  if (recorded) *recorded = region_recorded_[idx];
+  if (executed) *executed = region_executed_[idx];
+}
+
+// NVTX label of launch k of n: its width and the regions its gates come from
+// (most gates first), e.g. "cvm level 3/9: 7104 gates [adder/carry 6656, ...]".
+std::string GpuBackend::level_label(size_t k, size_t n, const std::vector<Bit>& ids) const {
+  std::vector<std::pair<uint64_t, uint32_t>> hist;
+  for (Bit id : ids) {
+    const uint32_t r = nodes_[id - 1].region;
+    auto it = std::find_if(hist.begin(), hist.end(), [r](const auto& h) { return h.second == r; });
+    if (it == hist.end()) hist.push_back({1, r});
+    else ++it->first;
+  }
+  std::sort(hist.begin(), hist.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::string s = "cvm level " + std::to_string(k + 1) + "/" + std::to_string(n) + ": " +
+                  std::to_string(ids.size()) + " gates [";
+  for (size_t i = 0; i < hist.size() && i < 3; ++i)
+    s += (i ? ", " : "") + (region_names_[hist[i].second].empty()
+                                ? std::string("-")
+                                : region_names_[hist[i].second]) +
+         " " + std::to_string(hist[i].first);
+  return s + (hist.size() > 3 ? ", ...]" : "]");
 }
 
 void GpuBackend::fence() {

@@ -1,6 +1,7 @@
 // extern "C" wrappers (include/cvm_gpu.h).  Exceptions become status codes
 // and a thread-local message, mirroring the reference's InputError / Error
 // split (errors.hpp:24-58).
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -428,6 +429,28 @@ int cvm_backend_stats_get(const cvm_backend* b, cvm_backend_stats* out) {
     *out = b->gpu ? b->gpu->stats() : b->clear->stats();
   });
 }
+int cvm_backend_region_count(const cvm_backend* b, uint64_t* out) {
+  return guard([&] {
+    need(b, "backend");
+    need(out, "out");
+    if (!b->gpu) throw InputError("the cleartext recorder keeps no region attribution");
+    *out = b->gpu->region_count();
+  });
+}
+int cvm_backend_region_info(const cvm_backend* b, uint64_t idx, char* name, size_t name_size,
+                            uint64_t* recorded, uint64_t* executed) {
+  return guard([&] {
+    need(b, "backend");
+    if (!b->gpu) throw InputError("the cleartext recorder keeps no region attribution");
+    std::string n;
+    b->gpu->region_info(idx, &n, recorded, executed);
+    if (name && name_size) {
+      const size_t k = std::min(n.size(), name_size - 1);
+      std::memcpy(name, n.data(), k);
+      name[k] = 0;
+    }
+  });
+}
 int cvm_backend_node_count(const cvm_backend* b, uint64_t* out) {
   return guard([&] {
     need(b, "backend");
@@ -506,7 +529,7 @@ int cvm_backend_evaluate(cvm_backend* b, size_t n, const cvm_handle* hs) {
   return guard([&] {
     need(b, "backend");
     if (n) need(hs, "handles");
-    if (b->gpu) b->gpu->flush_for(n, hs);
+    if (b->gpu) b->gpu->evaluate(n, hs);
   });
 }
 

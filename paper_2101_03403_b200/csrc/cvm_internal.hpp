@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -135,6 +136,7 @@ struct Node {
   int32_t sign;
   uint32_t constant;
   uint32_t plan;        // 1-based index of the captured plan producing it, 0 = none
+  uint32_t region;      // region path index at recording (GpuBackend::region_name)
 };
 
 class GpuBackend final : public Backend {
@@ -160,12 +162,21 @@ class GpuBackend final : public Backend {
   bool release_slots();
   void flush();                             // everything pending
   void flush_for(size_t n, const Bit* hs);  // cone of influence of hs only (validated)
+  // flush_for + one download of the requested gate outputs into a host cache:
+  // the key owner's bit-by-bit decryptions that follow (word.cpp:70-77) are
+  // then served without a device round trip each (cvm_backend_evaluate).
+  void evaluate(size_t n, const Bit* hs);
   // Flush policy of decrypt/export: the requested cone only (default) or
   // everything pending (for callers that decrypt bit by bit, like the
   // reference's decrypt_word loop, word.cpp:70-77).
   void set_cone_only(bool on) { cone_only_ = on; }
   Plan* capture_plan();
   cvm_backend_stats stats() const;
+  // Region attribution (the reference's region labels, GateDag::intern_region
+  // / bootstrapped_in_region, dag.hpp): path "a/b" of the region stack at
+  // each gate; index 0 = outside any region.
+  size_t region_count() const;
+  void region_info(size_t idx, std::string* name, uint64_t* recorded, uint64_t* executed) const;
   const std::vector<Node>& nodes() const { return nodes_; }
 
  private:
@@ -175,8 +186,13 @@ class GpuBackend final : public Backend {
   cvm_operand operand(Bit h) const;
   uint64_t take_slot();
   void stage_uploads();
-  std::vector<std::vector<cvm_gate>> levels_of(const std::vector<Bit>& ids) const;
-  std::vector<std::vector<cvm_gate>> pack_levels(std::vector<Bit> ids, uint32_t depth) const;
+  // launches of the selected gates; `ids_out` (optional) gets each launch's
+  // node ids in the same order
+  std::vector<std::vector<cvm_gate>> levels_of(const std::vector<Bit>& ids,
+                                               std::vector<std::vector<Bit>>* ids_out) const;
+  std::vector<std::vector<cvm_gate>> pack_levels(std::vector<Bit> ids, uint32_t depth,
+                                                 std::vector<std::vector<Bit>>* ids_out) const;
+  std::string level_label(size_t k, size_t n, const std::vector<Bit>& ids) const;
   void run(const std::vector<Bit>& ids);
   void retire(const std::vector<Bit>& done);
   void flush_locked();
@@ -198,10 +214,19 @@ class GpuBackend final : public Backend {
   std::vector<Bit> pending_;        // not yet evaluated gate nodes, id order
   uint64_t first_pending_ = UINT64_MAX;
   bool cone_only_ = true;
-  std::vector<std::string> regions_;
+  std::vector<uint32_t> region_stack_;        // indices of the open regions
+  std::vector<std::string> region_names_{""};  // interned paths
+  std::vector<uint64_t> region_recorded_{0}, region_executed_{0};
   uint64_t fences_ = 0;
   cvm_backend_stats stats_{};
   std::vector<std::shared_ptr<std::atomic<bool>>> plans_;  // captured plans: ran yet?
+  // Host copies of evaluated gate outputs (slot -> 631 words).  Only slots a
+  // flush of this backend wrote: gate outputs are never rewritten (a plan's
+  // and an input's slots are, so they are never cached); cleared when the
+  // backend returns its slots.
+  std::vector<uint8_t> slot_evaluated_;  // by slot - slot_base_
+  uint64_t slot_base_ = 0;
+  std::unordered_map<int64_t, std::vector<uint32_t>> cache_;
 };
 
 // Cleartext recorder: the SimBackend semantics (sim_backend.cpp:25-154) with

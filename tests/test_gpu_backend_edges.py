@@ -145,3 +145,49 @@ def test_plan_rejects_foreign_context(keyset, ctx):
         other.close()
     plan.run(ctx)  # its own context still works
     ctx.sync()
+
+
+def test_region_attribution(keyset, ctx):
+    """Gates carry the region path open at recording (push_region /
+    pop_region, as GateDag does); executed counts follow demand-driven
+    evaluation (dead gates stay unexecuted)."""
+    bk = P.Backend(ctx, keyset)
+    a, b = bk.encrypt_bit(1), bk.encrypt_bit(0)
+    bk.push_region("adder")
+    g1 = bk.binary_gate("AND", a, b)
+    bk.push_region("carry")
+    g2 = bk.binary_gate("OR", g1, a)
+    bk.pop_region()
+    bk.push_region("carry")  # the same path is interned once
+    bk.binary_gate("XOR", g2, b)
+    bk.pop_region()
+    bk.pop_region()
+    bk.binary_gate("NAND", a, b)
+    r = bk.regions()
+    assert r == {"": (1, 0), "adder": (1, 0), "adder/carry": (2, 0)}
+    assert bk.decrypt_bit(g2) is True
+    r = bk.regions()
+    assert r == {"": (1, 0), "adder": (1, 1), "adder/carry": (2, 1)}
+
+
+def test_evaluate_serves_bitwise_decrypts_from_host(keyset, ctx):
+    """cvm_backend_evaluate flushes the cone once and keeps the values on the
+    host: the reference's bit-by-bit decrypt_word (word.cpp:70-77) then runs
+    with no further flush, and the cached words equal the device slots."""
+    bk = P.Backend(ctx, keyset)
+    a = bk.import_lwe(keyset.encrypt_words([0xBEEF], 16, 61)[0])
+    b = bk.import_lwe(keyset.encrypt_words([0x1234], 16, 62)[0])
+    out = fu(bk, "add", a, b)
+    bk.evaluate(out)
+    st0 = bk.stats()
+    bits = [bk.decrypt_bit(int(h)) for h in out]
+    st1 = bk.stats()
+    assert st1["flushes"] == st0["flushes"] == 1
+    assert sum(int(x) << i for i, x in enumerate(bits)) == 0xBEEF + 0x1234
+    got = bk.export_lwe(out)  # from the cache
+    for h, row in zip(out, got):
+        slot, sign, const = bk.handle_slot(int(h))
+        dev = ctx.download(slot, 1)[0].astype(np.int64)
+        want = (sign * dev) % 2**32
+        want[630] = (want[630] + const) % 2**32
+        assert np.array_equal(row, want.astype(np.uint32))
