@@ -239,6 +239,29 @@ void cvmref_dag_free(cvmref_dag* d) {
   d->outputs = nullptr;
 }
 
+int cvmref_sim_program(unsigned word_size, unsigned register_count, const uint64_t* mem,
+                       uint64_t n_mem, const cvmref_insn* program, uint64_t n_insn,
+                       uint64_t max_steps, uint64_t* regs_out, uint8_t* nzcv_out) {
+  return guard([&] {
+    if ((n_mem && !mem) || (n_insn && !program) || !regs_out || !nzcv_out)
+      throw InputError("null argument");
+    const Program prog = to_program(word_size, program, n_insn);
+    SimBackend bk;
+    std::vector<Word> words;
+    for (uint64_t i = 0; i < n_mem; ++i) words.push_back(Word::encrypt(bk, mem[i], word_size));
+    LocalBranchOracle oracle(bk);
+    Machine m(bk, {.word_size = word_size, .register_count = register_count},
+              std::make_unique<BufferMemory>(word_size, std::move(words)), oracle);
+    m.run(prog, max_steps);
+    for (unsigned r = 0; r < register_count; ++r) regs_out[r] = decrypt_word(bk, m.reg(r));
+    const alu::Flags& f = m.flags();
+    nzcv_out[0] = bk.decrypt_bit(f.n);
+    nzcv_out[1] = bk.decrypt_bit(f.z);
+    nzcv_out[2] = bk.decrypt_bit(f.c);
+    nzcv_out[3] = bk.decrypt_bit(f.v);
+  });
+}
+
 int cvmref_sim_fu_batch(const char* op, unsigned width, uint64_t batch, const uint64_t* a,
                         const uint64_t* b, const uint64_t* c, uint64_t* out, double* seconds,
                         uint64_t* nodes) {

@@ -91,6 +91,14 @@ CVMREF_API int cvmref_record_program(unsigned word_size, unsigned register_count
                                      uint64_t n_insn, cvmref_dag* out);
 CVMREF_API void cvmref_dag_free(cvmref_dag* dag);
 
+/* The reference Machine on SimBackend (cleartext; LocalBranchOracle) over a
+ * BufferMemory holding mem[0..n_mem): the expected final registers and NZCV
+ * of a program, for cross-checks of the GPU against the reference. */
+CVMREF_API int cvmref_sim_program(unsigned word_size, unsigned register_count,
+                                  const uint64_t* mem, uint64_t n_mem,
+                                  const cvmref_insn* program, uint64_t n_insn,
+                                  uint64_t max_steps, uint64_t* regs_out, uint8_t* nzcv_out);
+
 /* The reference's own CPU path on the same circuit: `batch` instances of `op`
  * on SimBackend (cleartext booleans, sim_backend.cpp -- not FHE work),
  * operands a[i], b[i] (and c[i] for add_cin / addsub); results decrypted as

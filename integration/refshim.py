@@ -59,10 +59,11 @@ def lib():
         L.cvmref_sim_fu_batch.argtypes = [ctypes.c_char_p, u32, u64, p, p, p, p,
                                           ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_uint64)]
+        L.cvmref_sim_program.argtypes = [u32, u32, p, u64, p, u64, u64, p, p]
         L.cvmref_add_batch_gpu.argtypes = [p, p, u32, u64, p, p, p, p, p]
         L.cvmref_run_program_gpu.argtypes = [p, p, u32, u32, p, u64, p, u64, u64, p, p, p, p]
         for f in ("cvmref_record_fu", "cvmref_record_program", "cvmref_add_batch_gpu",
-                  "cvmref_sim_fu_batch",
+                  "cvmref_sim_fu_batch", "cvmref_sim_program",
                   "cvmref_run_program_gpu"):
             getattr(L, f).restype = i
         _LIB = L
@@ -117,6 +118,72 @@ def record_program(program, n_mem, word_size=16, register_count=8):
     _check(lib().cvmref_record_program(word_size, register_count, n_mem, _insns(program),
                                        len(program), ctypes.byref(d)))
     return _to_dag(d, "program")
+
+
+def sim_program(program, mem, word_size=16, register_count=8, max_steps=None):
+    """The reference Machine on SimBackend: (final registers, NZCV)."""
+    mem = np.ascontiguousarray(mem, np.uint64)
+    regs = np.zeros(register_count, np.uint64)
+    nzcv = np.zeros(4, np.uint8)
+    steps = max_steps if max_steps is not None else 10 * len(program) + 1
+    _check(lib().cvmref_sim_program(word_size, register_count, mem.ctypes.data, len(mem),
+                                    _insns(program), len(program), steps, regs.ctypes.data,
+                                    nzcv.ctypes.data))
+    return regs, nzcv
+
+
+def random_program(rng, width, count=16, n_mem=4, n_regs=8):
+    """A seeded straight-line program over the whole data-path ISA (isa.hpp:
+    MOV/LOAD/STORE, ADD(S)/SUB(S) with register or immediate operands,
+    MUL/SMULS/UDIV, shifts by register or immediate, the bitwise ops, NOT,
+    BFC/BFI/RBIT/REV, CMP) -- the shape of the reference's random-program
+    cross-check (emulator_test.cc:486-640), generated here."""
+    mask = (1 << width) - 1
+    reg = lambda: int(rng.integers(n_regs))  # noqa: E731
+    out = []
+    for _ in range(count):
+        k = int(rng.integers(16))
+        x = dict(rd=-1, rn=-1, rm=-1)
+        if k == 0:
+            x.update(op="MOV", rd=reg(), has_imm=1, imm=int(rng.integers(mask + 1)))
+        elif k == 1:
+            x.update(op="LOAD", rd=reg(), has_imm=1, imm=int(rng.integers(n_mem)))
+        elif k == 2:
+            x.update(op="STORE", rn=reg(), has_imm=1, imm=int(rng.integers(n_mem)))
+        elif k in (3, 4):
+            x.update(op=["ADDS", "SUBS"][k - 3], rd=reg(), rn=reg(), sets_flags=1)
+            if rng.integers(2):
+                x.update(has_imm=1, imm=int(rng.integers(mask + 1)))
+            else:
+                x.update(rm=reg())
+        elif k == 5:
+            x.update(op=["MUL", "SMULS"][int(rng.integers(2))], rd=reg(), rn=reg(), rm=reg())
+            x["sets_flags"] = int(x["op"] == "SMULS")
+        elif k == 6:
+            x.update(op="UDIV", rd=reg(), rn=reg(), rm=reg())
+        elif k == 7:
+            x.update(op=["LLS", "LRS", "ARS"][int(rng.integers(3))], rd=reg(), rn=reg())
+            if rng.integers(2):
+                x.update(has_imm=1, imm=int(rng.integers(width + 1)))
+            else:
+                x.update(rm=reg())
+        elif k in (8, 9, 10, 11):
+            x.update(op=["AND", "OR", "XOR", "ORN"][k - 8], rd=reg(), rn=reg(), rm=reg())
+        elif k == 12:
+            x.update(op="NOT", rd=reg(), rn=reg())
+        elif k == 13:
+            lsb = int(rng.integers(width))
+            wd = 1 + int(rng.integers(width - lsb))
+            x.update(op=["BFC", "BFI"][int(rng.integers(2))], rd=reg(), has_imm=1, imm=lsb,
+                     has_imm2=1, imm2=wd)
+            if x["op"] == "BFI":
+                x["rn"] = reg()
+        elif k == 14:
+            x.update(op=["RBIT", "REV"][int(rng.integers(2))], rd=reg(), rn=reg())
+        else:
+            x.update(op="CMP", rn=reg(), rm=reg(), sets_flags=1)
+        out.append(x)
+    return out
 
 
 def sim_fu_batch(op, width, a, b, c=None):

@@ -75,7 +75,7 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
 
 
 @pytest.mark.parametrize("n", [700, 1224, 1584, 1984])
-def test_wide_level_planner_bit_identical(n, keyset, ctx):
+def test_wide_level_planner_bit_identical(n, keyset, ctx, oracle_keys):
     """Auto selection of a wide level: full waves of the v4 warp kernel, then
     the remainder on another v4 wave with fewer warps per SM, on v3 rounds
     and/or latency rounds (blind_rotate.cu).  The sizes hit each combination;
@@ -101,9 +101,14 @@ def test_wide_level_planner_bit_identical(n, keyset, ctx):
     auto, ref = ctx.download(base + 2 * n, n), ctx.download(base + 3 * n, n)
     assert np.array_equal(auto, ref)
     assert np.array_equal(keyset.decrypt(auto), a & b)
+    # not only self-consistent: a sample spread over every kernel of the
+    # plan (head waves, remainder kernels) against the exact oracle
+    idx = np.unique(np.concatenate([np.arange(0, n, max(1, n // 24)), [n - 1]]))
+    want = oracle_keys.gates(np.full(len(idx), O.AND, np.uint8), ca[idx], cb[idx])
+    assert np.array_equal(auto[idx], want)
 
 
-def test_wide_mux_level_auto_vs_pinned(keyset, ctx):
+def test_wide_mux_level_auto_vs_pinned(keyset, ctx, oracle_keys):
     """A wide MUX level (700 gates = 1,400 blind rotations: a full v4 wave plus
     a remainder, then the split-K key switch over 6 tiles with two extracted
     samples per gate) under the auto selection equals the same level on
@@ -132,6 +137,9 @@ def test_wide_mux_level_auto_vs_pinned(keyset, ctx):
     auto, pinned = ctx.download(base + 3 * n, n), ctx.download(base + 4 * n, n)
     assert np.array_equal(auto, pinned)
     assert np.array_equal(keyset.decrypt(auto), np.where(s == 1, t, f))
+    idx = np.unique(np.concatenate([np.arange(0, n, 29), [n - 1]]))
+    want = oracle_keys.gates(np.full(len(idx), O.MUX, np.uint8), cs[idx], ct[idx], cf[idx])
+    assert np.array_equal(auto[idx], want)
 
 
 @pytest.mark.parametrize("op", ["add", "cmp"])
