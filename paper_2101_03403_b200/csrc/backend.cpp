@@ -89,6 +89,9 @@ Bit GpuBackend::record_gate(Node n, const cvm_gate& g) {
 
 Bit GpuBackend::constant(bool value) {
   std::lock_guard<std::mutex> lock(mu_);
+  return constant_nl(value);
+}
+Bit GpuBackend::constant_nl(bool value) {
   Node n{};
   n.kind = GateKind::Constant;
   n.const_value = value;
@@ -100,6 +103,9 @@ Bit GpuBackend::constant(bool value) {
 
 Bit GpuBackend::unary_gate(GateKind kind, Bit a) {
   std::lock_guard<std::mutex> lock(mu_);
+  return unary_gate_nl(kind, a);
+}
+Bit GpuBackend::unary_gate_nl(GateKind kind, Bit a) {
   if (kind != GateKind::Not && kind != GateKind::Copy)
     throw InputError("not a unary gate");
   const Node& in = node(a, "unary_gate");
@@ -119,6 +125,9 @@ Bit GpuBackend::unary_gate(GateKind kind, Bit a) {
 
 Bit GpuBackend::binary_gate(GateKind kind, Bit a, Bit b) {
   std::lock_guard<std::mutex> lock(mu_);
+  return binary_gate_nl(kind, a, b);
+}
+Bit GpuBackend::binary_gate_nl(GateKind kind, Bit a, Bit b) {
   const Node& na = node(a, "binary_gate");
   const Node& nb = node(b, "binary_gate");
   if (bootstrap_count(kind) != 1) throw InputError("not a bootstrapped binary gate");
@@ -141,6 +150,9 @@ Bit GpuBackend::binary_gate(GateKind kind, Bit a, Bit b) {
 
 Bit GpuBackend::mux_gate(Bit sel, Bit on_true, Bit on_false) {
   std::lock_guard<std::mutex> lock(mu_);
+  return mux_gate_nl(sel, on_true, on_false);
+}
+Bit GpuBackend::mux_gate_nl(Bit sel, Bit on_true, Bit on_false) {
   const Node& ns = node(sel, "mux_gate");
   const Node& nt = node(on_true, "mux_gate");
   const Node& nf = node(on_false, "mux_gate");
@@ -160,6 +172,26 @@ Bit GpuBackend::mux_gate(Bit sel, Bit on_true, Bit on_false) {
   g.in[2] = operand(on_false);
   g.out_slot = uint64_t(n.slot);
   return record_gate(n, g);
+}
+
+// A recorded table replayed under one lock (dag.cpp validates it first).
+void GpuBackend::replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs,
+                        Bit* handles) {
+  std::lock_guard<std::mutex> lock(mu_);
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const cvm_dag_node& d = nodes[i];
+    const GateKind kind = GateKind(d.kind);
+    Bit h;
+    if (d.input) h = inputs[k++];
+    else if (kind == GateKind::Constant) h = constant_nl(d.value != 0);
+    else if (kind == GateKind::Not || kind == GateKind::Copy)
+      h = unary_gate_nl(kind, handles[d.dep[0] - 1]);
+    else if (kind == GateKind::Mux)
+      h = mux_gate_nl(handles[d.dep[0] - 1], handles[d.dep[1] - 1], handles[d.dep[2] - 1]);
+    else h = binary_gate_nl(kind, handles[d.dep[0] - 1], handles[d.dep[1] - 1]);
+    handles[i] = h;
+  }
 }
 
 Bit GpuBackend::encrypt_bit(bool value) {

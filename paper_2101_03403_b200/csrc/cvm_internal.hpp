@@ -153,6 +153,8 @@ class GpuBackend final : public Backend {
   void fence() override;
 
   void decrypt_bits(size_t n, const Bit* hs, uint8_t* out);
+  // a validated recorded table (dag.cpp) re-issued under one lock
+  void replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs, Bit* handles);
   void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
   void import_lwe_direct(size_t n, const uint32_t* lwe, Bit* out);
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
@@ -181,6 +183,10 @@ class GpuBackend final : public Backend {
 
  private:
   const Node& node(Bit h, const char* what) const;
+  Bit constant_nl(bool value);  // the gate calls without taking mu_
+  Bit unary_gate_nl(GateKind kind, Bit a);
+  Bit binary_gate_nl(GateKind kind, Bit a, Bit b);
+  Bit mux_gate_nl(Bit sel, Bit on_true, Bit on_false);
   Bit add_node(Node n);
   Bit record_gate(Node n, const cvm_gate& g);
   cvm_operand operand(Bit h) const;

@@ -43,6 +43,10 @@ void replay_dag(Backend& bk, const cvm_dag_node* nodes, uint64_t n, const Bit* i
     throw InputError("dag has " + std::to_string(need) + " input nodes, " +
                      std::to_string(n_inputs) + " inputs given");
   if (n && !handles) throw InputError("null handle output");
+  if (auto* gpu = dynamic_cast<GpuBackend*>(&bk)) {
+    gpu->replay(nodes, n, inputs, handles);  // one lock for the whole table
+    return;
+  }
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const cvm_dag_node& d = nodes[i];
