@@ -142,11 +142,17 @@ std::vector<BitHandle> build_fu(Backend& bk, const std::string& op, unsigned wid
 
 void fill(const DagRecorder& rec, const std::vector<BitHandle>& outs, cvmref_dag* out) {
   const std::vector<cvm_dag_node> t = rec.table();
+  auto* nodes = static_cast<cvm_dag_node*>(std::malloc(sizeof(cvm_dag_node) * (t.size() + 1)));
+  auto* outputs = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (outs.size() + 1)));
+  if (!nodes || !outputs) {
+    std::free(nodes);
+    std::free(outputs);
+    throw std::bad_alloc();
+  }
   out->n_nodes = t.size();
-  out->nodes = static_cast<cvm_dag_node*>(std::malloc(sizeof(cvm_dag_node) * (t.size() + 1)));
+  out->nodes = nodes;
   out->n_outputs = outs.size();
-  out->outputs = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (outs.size() + 1)));
-  if (!out->nodes || !out->outputs) throw std::bad_alloc();
+  out->outputs = outputs;
   std::memcpy(out->nodes, t.data(), sizeof(cvm_dag_node) * t.size());
   out->n_inputs = 0;
   for (const cvm_dag_node& n : t) out->n_inputs += n.input;

@@ -13,7 +13,7 @@ from paper_2101_03403_b200._native import check, lib  # noqa: E402
 
 def main():
     n = int(os.environ.get("N", 6))
-    variants = [int(v) for v in os.environ.get("VARIANTS", "3044,9,13,23,1").split(",")]
+    variants = [int(v) for v in os.environ.get("VARIANTS", "6015,5247,9,96").split(",")]
     ks = P.KeySet(3)
     ctx = P.Context(0)
     ctx.upload_keyset(ks)
@@ -24,7 +24,7 @@ def main():
         ctx.upload(base + k * n, ks.encrypt(bits, 10 + k))
     for v in variants:
         check(lib.cvm_set_br_variant(v))
-        for kv in (1, 6):
+        for kv in (8, 9):
             check(lib.cvm_set_ks_variant(kv))
             ctx.submit_level([("MUX", [(base + i, 1, 0), (base + n + i, 1, 0),
                                        (base + 2 * n + i, 1, 0)], base + 3 * n + i)
