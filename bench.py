@@ -222,8 +222,19 @@ def cpu_baseline():
     threads = os.cpu_count() or 1
     adders = int(os.environ.get("CPU_ADDERS", max(4, threads)))
     rate, dt, gates, ok = cpu_add16_circuits(adders, threads)
+    # one bootstrap on one thread, for comparison with the paper's single-core
+    # 25.6 ms per gate (a 2014 Xeon core with the TFHE
+    # library's AVX FFT)
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    sk = O.SecretKeys(KEY_SEED)
+    ck = O.CloudKeys(sk.bk, sk.ksk, O.MODE_FFT)
+    a1, b1 = sk.encrypt(np.array([1, 0], np.uint8), 3), sk.encrypt(np.array([1, 1], np.uint8), 4)
+    t = time.perf_counter()
+    ck.gates(np.array([O.AND, O.XOR], np.uint8), a1, b1, None, 1)
+    one = (time.perf_counter() - t) / 2
     return {"value": rate, "unit": "bootstrapped gates/s", "cores": threads, "kind": "port",
-            "seconds": dt, **info,
+            "seconds": dt, **info, "single_thread_ms_per_gate": 1e3 * one,
             "sample": f"{adders} whole ADD16 circuits ({gates} bootstrapped gates, all 9 "
                       f"levels, adders in lockstep per level), oracle/ double-FFT TFHE "
                       f"(the TFHE library's method), {threads} threads",
