@@ -283,7 +283,8 @@ typedef struct cvm_dag_node {
   uint8_t value;    /* CONSTANT: the constant bit                          */
   uint8_t ndeps;    /* DagNode::dep_count: 0 (CONSTANT, input), 1 (NOT,    */
                     /*    COPY), 2 (binary gates), 3 (MUX: sel, t, f)      */
-  uint32_t pad;
+  uint32_t region;  /* DagNode::region: index into the table's region     */
+                    /*    names (GateDag::regions()), 0 = none             */
   uint64_t dep[3];  /* DagNode::dep: ids of earlier nodes                  */
 } cvm_dag_node;
 
@@ -294,6 +295,12 @@ typedef struct cvm_dag_node {
 CVM_API int cvm_backend_replay_dag(cvm_backend* b, const cvm_dag_node* nodes,
                                    uint64_t n_nodes, const cvm_handle* inputs,
                                    uint64_t n_inputs, cvm_handle* handles);
+/* Region names of the tables replayed next on `b` (names[k] for region index
+ * k of a node; names[0] is the unlabelled ""): replayed gates are then
+ * attributed to those paths (cvm_backend_region_info, NVTX labels).  n = 0
+ * clears them. */
+CVM_API int cvm_backend_set_dag_regions(cvm_backend* b, const char* const* names,
+                                        uint64_t n);
 /* Evaluate the cone of influence of `count` handles now (one flush) and
  * download their values once into a host cache, so the key owner's later
  * bit-by-bit decryptions (word.cpp:70-77) need no device round trip each. */
@@ -310,6 +317,14 @@ CVM_API int cvm_dag_batch(cvm_ctx* ctx, const cvm_dag_node* nodes, uint64_t n_no
                           const uint64_t* outputs, uint64_t n_outputs, uint64_t batch,
                           const uint32_t* in_lwe, uint64_t in_words, uint32_t* out_lwe,
                           uint64_t out_words, cvm_backend_stats* stats);
+/* The same with the table's region names (see cvm_backend_set_dag_regions),
+ * so the batch's launches carry NVTX labels of the reference's regions. */
+CVM_API int cvm_dag_batch_regions(cvm_ctx* ctx, const cvm_dag_node* nodes, uint64_t n_nodes,
+                                  const char* const* region_names, uint64_t n_regions,
+                                  const uint64_t* outputs, uint64_t n_outputs,
+                                  uint64_t batch, const uint32_t* in_lwe, uint64_t in_words,
+                                  uint32_t* out_lwe, uint64_t out_words,
+                                  cvm_backend_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -51,6 +51,7 @@ std::vector<cvm_dag_node> DagRecorder::table() const {
     d.input = n.input ? 1 : 0;
     d.ndeps = n.dep_count;
     d.value = n.id < const_value_.size() ? const_value_[n.id] : 0;
+    d.region = n.region;
     for (int j = 0; j < 3; ++j) d.dep[j] = n.dep[j];
   }
   return t;
@@ -156,6 +157,15 @@ void fill(const DagRecorder& rec, const std::vector<BitHandle>& outs, cvmref_dag
   std::memcpy(out->nodes, t.data(), sizeof(cvm_dag_node) * t.size());
   out->n_inputs = 0;
   for (const cvm_dag_node& n : t) out->n_inputs += n.input;
+  const auto names = rec.dag().regions();
+  out->n_regions = names.size();
+  out->regions = static_cast<char**>(std::calloc(names.size() + 1, sizeof(char*)));
+  if (!out->regions) throw std::bad_alloc();
+  for (std::size_t k = 0; k < names.size(); ++k) {
+    out->regions[k] = static_cast<char*>(std::malloc(names[k].size() + 1));
+    if (!out->regions[k]) throw std::bad_alloc();
+    std::memcpy(out->regions[k], names[k].c_str(), names[k].size() + 1);
+  }
   for (std::size_t i = 0; i < outs.size(); ++i) out->outputs[i] = outs[i].node();
 }
 
@@ -241,8 +251,12 @@ void cvmref_dag_free(cvmref_dag* d) {
   if (!d) return;
   std::free(d->nodes);
   std::free(d->outputs);
+  if (d->regions)
+    for (uint64_t k = 0; k < d->n_regions; ++k) std::free(d->regions[k]);
+  std::free(d->regions);
   d->nodes = nullptr;
   d->outputs = nullptr;
+  d->regions = nullptr;
 }
 
 int cvmref_sim_program(unsigned word_size, unsigned register_count, const uint64_t* mem,

@@ -61,6 +61,8 @@ typedef struct cvmref_dag {
   uint64_t* outputs;
   uint64_t n_outputs;
   uint64_t n_inputs;
+  char** regions;  /* GateDag::regions(): path of each node.region index */
+  uint64_t n_regions;
 } cvmref_dag;
 
 /* One instruction of a straight-line or branching program (isa.hpp:87-97).

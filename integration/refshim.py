@@ -24,7 +24,8 @@ FU_OPS = ["add", "add_cin", "sub", "addsub", "cmp", "and", "orr", "eor", "orn", 
 class RefDag(ctypes.Structure):
     _fields_ = [("nodes", ctypes.c_void_p), ("n_nodes", ctypes.c_uint64),
                 ("outputs", ctypes.POINTER(ctypes.c_uint64)), ("n_outputs", ctypes.c_uint64),
-                ("n_inputs", ctypes.c_uint64)]
+                ("n_inputs", ctypes.c_uint64), ("regions", ctypes.POINTER(ctypes.c_char_p)),
+                ("n_regions", ctypes.c_uint64)]
 
 
 class RefInsn(ctypes.Structure):
@@ -83,8 +84,9 @@ def _to_dag(d, name):
                           dtype=P.DAG_DTYPE).copy()
     outs = np.ctypeslib.as_array(d.outputs, shape=(d.n_outputs,)).copy() \
         if d.n_outputs else np.zeros(0, np.uint64)
+    regions = [d.regions[k].decode() for k in range(d.n_regions)]
     lib().cvmref_dag_free(ctypes.byref(d))
-    return P.Dag(nodes, outs, name)
+    return P.Dag(nodes, outs, name, regions)
 
 
 def record_fu(op, width):

@@ -65,7 +65,7 @@ class BackendStats(ctypes.Structure):
 class DagNode(ctypes.Structure):
     """cvm_dag_node: one node of a recorded circuit (the reference DagNode)."""
     _fields_ = [("kind", ctypes.c_uint8), ("input", ctypes.c_uint8), ("value", ctypes.c_uint8),
-                ("ndeps", ctypes.c_uint8), ("pad", ctypes.c_uint32),
+                ("ndeps", ctypes.c_uint8), ("region", ctypes.c_uint32),
                 ("dep", ctypes.c_uint64 * 3)]
 
 
@@ -144,6 +144,9 @@ _SIGS = {
                                      ctypes.POINTER(ctypes.c_uint32)]),
     "cvm_backend_replay_dag": (_i, [_p, _p, _u64, _p, _u64, _p]),
     "cvm_backend_evaluate": (_i, [_p, ctypes.c_size_t, _p]),
+    "cvm_backend_set_dag_regions": (_i, [_p, _p, _u64]),
+    "cvm_dag_batch_regions": (_i, [_p, _p, _u64, _p, _u64, _p, _u64, _u64, _p, _u64, _p, _u64,
+                                   ctypes.POINTER(BackendStats)]),
     "cvm_dag_batch": (_i, [_p, _p, _u64, _p, _u64, _u64, _p, _u64, _p, _u64,
                            ctypes.POINTER(BackendStats)]),
 }

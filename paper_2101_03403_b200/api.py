@@ -19,7 +19,7 @@ KIND = {n: i for i, n in enumerate(GATE_KINDS)}
 
 # cvm_dag_node (include/cvm_gpu.h): 32 bytes per node
 DAG_DTYPE = np.dtype([("kind", "u1"), ("input", "u1"), ("value", "u1"), ("ndeps", "u1"),
-                      ("pad", "<u4"), ("dep", "<u8", (3,))])
+                      ("region", "<u4"), ("dep", "<u8", (3,))])
 assert DAG_DTYPE.itemsize == ctypes.sizeof(N.DagNode)
 
 
@@ -28,10 +28,18 @@ class Dag:
     1-based in creation order) plus each CONSTANT's value, and the ids of its
     output bits (LSB first).  Inputs are the input nodes in id order."""
 
-    def __init__(self, nodes, outputs, name=""):
+    def __init__(self, nodes, outputs, name="", regions=None):
         self.nodes = np.ascontiguousarray(nodes, dtype=DAG_DTYPE)
         self.outputs = np.ascontiguousarray(outputs, dtype=np.uint64)
         self.name = name
+        # region path of each node.region index (GateDag::regions(); [0] = "")
+        self.regions = list(regions) if regions else None
+
+    def _region_array(self):
+        if not self.regions:
+            return None, 0
+        arr = (ctypes.c_char_p * len(self.regions))(*[r.encode() for r in self.regions])
+        return arr, len(self.regions)
 
     @classmethod
     def from_rows(cls, rows, outputs, name=""):
@@ -365,6 +373,8 @@ class Backend:
         every node (index = node id - 1)."""
         inputs = np.ascontiguousarray(inputs, dtype=np.uint64).ravel()
         out = np.zeros(dag.n_nodes, np.uint64)
+        names, n = dag._region_array()
+        check(lib.cvm_backend_set_dag_regions(self._h, names, n))
         check(lib.cvm_backend_replay_dag(self._h, dag.nodes.ctypes.data, dag.n_nodes,
                                          _vp(inputs), len(inputs), _vp(out)))
         return out
@@ -419,7 +429,8 @@ def dag_batch(ctx, dag, in_lwe):
     batch = a.size // per
     out = np.empty((batch, len(dag.outputs), N.LWE_WORDS), np.uint32)
     st = N.BackendStats()
-    check(lib.cvm_dag_batch(ctx.handle, dag.nodes.ctypes.data, dag.n_nodes,
-                            _vp(dag.outputs), len(dag.outputs), batch, _vp(a), a.size,
-                            _vp(out), out.size, ctypes.byref(st)))
+    names, n = dag._region_array()
+    check(lib.cvm_dag_batch_regions(ctx.handle, dag.nodes.ctypes.data, dag.n_nodes, names, n,
+                                    _vp(dag.outputs), len(dag.outputs), batch, _vp(a), a.size,
+                                    _vp(out), out.size, ctypes.byref(st)))
     return out, st.as_dict()

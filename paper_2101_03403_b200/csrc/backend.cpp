@@ -191,6 +191,15 @@ void GpuBackend::replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs
       h = mux_gate_nl(handles[d.dep[0] - 1], handles[d.dep[1] - 1], handles[d.dep[2] - 1]);
     else h = binary_gate_nl(kind, handles[d.dep[0] - 1], handles[d.dep[1] - 1]);
     handles[i] = h;
+    // attribute the gate to the table's region (recorded as the stack's top
+    // otherwise)
+    if (!dag_region_.empty() && d.region && is_gate(kind) && !d.input) {
+      Node& nd = nodes_[h - 1];
+      if (d.region >= dag_region_.size()) throw InputError("dag region index out of range");
+      region_recorded_[nd.region]--;
+      nd.region = dag_region_[d.region];
+      region_recorded_[nd.region]++;
+    }
   }
 }
 
@@ -622,21 +631,31 @@ void GpuBackend::decrypt_bits(size_t count, const Bit* hs, uint8_t* out) {
   stats_.decrypts += count;
 }
 
+uint32_t GpuBackend::intern_region(const std::string& path) {
+  for (size_t i = 1; i < region_names_.size(); ++i)
+    if (region_names_[i] == path) return uint32_t(i);
+  region_names_.push_back(path);
+  region_recorded_.push_back(0);
+  region_executed_.push_back(0);
+  return uint32_t(region_names_.size() - 1);
+}
+
 void GpuBackend::push_region(std::string_view name) {
   std::lock_guard<std::mutex> lock(mu_);
-  std::string path = region_stack_.empty() ? std::string(name)
-                                           : region_names_[region_stack_.back()] + "/" +
-                                                 std::string(name);
-  uint32_t idx = 0;
-  for (size_t i = 1; i < region_names_.size() && !idx; ++i)
-    if (region_names_[i] == path) idx = uint32_t(i);
-  if (!idx) {
-    idx = uint32_t(region_names_.size());
-    region_names_.push_back(std::move(path));
-    region_recorded_.push_back(0);
-    region_executed_.push_back(0);
+  const std::string path = region_stack_.empty()
+                               ? std::string(name)
+                               : region_names_[region_stack_.back()] + "/" + std::string(name);
+  region_stack_.push_back(path.empty() ? 0u : intern_region(path));
+}
+
+void GpuBackend::set_dag_regions(const char* const* names, uint64_t n) {
+  std::lock_guard<std::mutex> lock(mu_);
+  dag_region_.assign(n, 0);
+  for (uint64_t k = 0; k < n; ++k) {
+    if (!names[k]) throw InputError("null region name");
+    const std::string path(names[k]);
+    dag_region_[k] = path.empty() ? 0u : intern_region(path);
   }
-  region_stack_.push_back(idx);
 }
 
 void GpuBackend::pop_region() {

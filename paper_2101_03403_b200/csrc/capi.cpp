@@ -525,6 +525,13 @@ int cvm_backend_replay_dag(cvm_backend* b, const cvm_dag_node* nodes, uint64_t n
     replay_dag(*b->impl, nodes, n, inputs, n_inputs, handles);
   });
 }
+int cvm_backend_set_dag_regions(cvm_backend* b, const char* const* names, uint64_t n) {
+  return guard([&] {
+    need(b, "backend");
+    if (n) need(names, "names");
+    if (b->gpu) b->gpu->set_dag_regions(names, n);
+  });
+}
 int cvm_backend_evaluate(cvm_backend* b, size_t n, const cvm_handle* hs) {
   return guard([&] {
     need(b, "backend");
@@ -537,6 +544,15 @@ int cvm_dag_batch(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_nodes,
                   const uint64_t* outputs, uint64_t n_outputs, uint64_t batch,
                   const uint32_t* in_lwe, uint64_t in_words, uint32_t* out_lwe,
                   uint64_t out_words, cvm_backend_stats* stats) {
+  return cvm_dag_batch_regions(c, nodes, n_nodes, nullptr, 0, outputs, n_outputs, batch, in_lwe,
+                               in_words, out_lwe, out_words, stats);
+}
+
+int cvm_dag_batch_regions(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_nodes,
+                          const char* const* region_names, uint64_t n_regions,
+                          const uint64_t* outputs, uint64_t n_outputs, uint64_t batch,
+                          const uint32_t* in_lwe, uint64_t in_words, uint32_t* out_lwe,
+                          uint64_t out_words, cvm_backend_stats* stats) {
   return guard([&] {
     need(c, "ctx");
     uint64_t n_in = 0;
@@ -555,6 +571,10 @@ int cvm_dag_batch(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_nodes,
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     GpuBackend bk(c->ctx, nullptr, 0);
+    if (n_regions) {
+      need(region_names, "region_names");
+      bk.set_dag_regions(region_names, n_regions);
+    }
     std::vector<Bit> in(batch * n_in), handles(n_nodes), outs(batch * n_outputs);
     // Inputs are DMA'd straight from the caller's buffers; every path out of
     // this call synchronises the stream first, so they may be released after.

@@ -155,6 +155,8 @@ class GpuBackend final : public Backend {
   void decrypt_bits(size_t n, const Bit* hs, uint8_t* out);
   // a validated recorded table (dag.cpp) re-issued under one lock
   void replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs, Bit* handles);
+  // region names of the replayed tables' node.region indices
+  void set_dag_regions(const char* const* names, uint64_t n);
   void import_lwe(size_t n, const uint32_t* lwe, Bit* out);
   void import_lwe_direct(size_t n, const uint32_t* lwe, Bit* out);
   void export_lwe(size_t n, const Bit* hs, uint32_t* out);
@@ -223,6 +225,8 @@ class GpuBackend final : public Backend {
   std::vector<uint32_t> region_stack_;        // indices of the open regions
   std::vector<std::string> region_names_{""};  // interned paths
   std::vector<uint64_t> region_recorded_{0}, region_executed_{0};
+  std::vector<uint32_t> dag_region_;  // replayed table's region index -> region id
+  uint32_t intern_region(const std::string& path);
   uint64_t fences_ = 0;
   cvm_backend_stats stats_{};
   std::vector<std::shared_ptr<std::atomic<bool>>> plans_;  // captured plans: ran yet?

@@ -191,3 +191,30 @@ def test_evaluate_serves_bitwise_decrypts_from_host(keyset, ctx):
         want = (sign * dev) % 2**32
         want[630] = (want[630] + const) % 2**32
         assert np.array_equal(row, want.astype(np.uint32))
+
+
+def test_recorded_table_keeps_reference_regions(keyset, ctx):
+    """A table recorded by the reference carries GateDag region indices and
+    names; replayed on the device, every bootstrapped gate is attributed to
+    its reference region path (the labels of the NVTX launch ranges)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "integration"))
+    import refshim
+    if not refshim.available():
+        pytest.skip("libcvm_refshim.so not built")
+    dag = refshim.record_fu("add", 16)
+    assert dag.regions[:2] == ["", "adder"] and "adder/sum" in dag.regions
+    bk = P.Backend(ctx, keyset)
+    ins = bk.import_lwe(np.concatenate([keyset.encrypt_words([7], 16, 71)[0],
+                                        keyset.encrypt_words([9], 16, 72)[0]]))
+    out = bk.replay_outputs(dag, ins)
+    gates = (dag.nodes["input"] == 0) & (dag.nodes["kind"] >= P.KIND["NAND"])
+    want = {}
+    for r, n in zip(*np.unique(dag.nodes["region"][gates], return_counts=True)):
+        want[dag.regions[r]] = int(n)
+    got = {k: v[0] for k, v in bk.regions().items() if v[0]}
+    assert got == want
+    assert bk.decrypt_word(out) == 16
+    assert sum(v[1] for v in bk.regions().values()) == bk.stats()["executed"]
