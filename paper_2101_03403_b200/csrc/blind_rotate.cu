@@ -540,9 +540,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
                &sm.full[g]);
     }
     __syncthreads();  // all three levels' partial products in red
-    if (g == 1) {     // the peer's polynomial: sum over levels, store remotely
+    if (g >= 1) {     // the peer's polynomial: sum over levels, store remotely
+      // (groups 1 and 2 take half the bins each: the peer's wait is shorter)
 #pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) {
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k2 = 4 * (g - 1) + kk;
         const c64 x = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
                            sm.red[2][r ^ 1][k2][t]);
         const uint32_t a = peer_recv_a + uint32_t(((i & 1) * 512 + k2 * 64 + t) * 16);
