@@ -28,6 +28,8 @@ HOST_FLAGS = ["-O2", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xptxas", "-v",
                      "--expt-relaxed-constexpr",
                      "-Xcompiler", ",".join(HOST_FLAGS)]
+# developer instrumentation builds only (e.g. CVM_NVCC_EXTRA=-DCVM_PHASE_PROF)
+NVCC_FLAGS += os.environ.get("CVM_NVCC_EXTRA", "").split()
 CXX_FLAGS = ["-std=c++20"] + HOST_FLAGS + ["-I/usr/local/cuda/include"]
 
 SOURCES = ["blind_rotate.cu", "blind_rotate_v4.cu", "key_switch.cu", "device_misc.cu", "context.cu", "keys.cpp",

@@ -441,6 +441,21 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
 // cluster barrier per CMux step; each CTA then runs one inverse transform and
 // updates its own ACC part -- no ACC broadcast is needed, because the digits
 // of part r depend only on ACC part r.
+#ifdef CVM_PHASE_PROF
+// Developer instrumentation (tools/pair_phases.py): per-phase clock64 sums
+// of thread 0 of groups 0 and 1 of every CTA, [cta][group][phase].
+__device__ unsigned long long g_pair_phase[148 * 2][2][12];
+#define PH(k)                                      \
+  do {                                             \
+    const long long now_ = clock64();              \
+    ph[k] += (unsigned long long)(now_ - last_);   \
+    last_ = now_;                                  \
+  } while (0)
+#else
+#define PH(k) \
+  do {        \
+  } while (0)
+#endif
 struct PairSmem {
   c64 bkbuf[kL][1024];    // 48 KB: this CTA's three TRGSW rows
   c64 xbuf[kL][2][512];   // 48 KB: two exchange buffers per group (no WAR barrier)
@@ -512,21 +527,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
   c64* xb1 = sm.xbuf[g][1];
   auto sync = [bar_id] { group_sync(bar_id); };
   cluster.sync();  // the peer's shared memory is live before any remote store
+#ifdef CVM_PHASE_PROF
+  unsigned long long ph[12] = {};
+  long long last_ = clock64();
+#endif
 
   for (int i = 0; i < kN; ++i) {
     __syncthreads();  // ACC part r of the previous step complete
+    PH(0);
     if (tid == 0) mbar_expect_tx(&sm.rbar[i & 1], 8 * 64 * 16);
     const int ai = sm.bar[i];
     uint32_t dif[16];
     rotated_diff(sm.acc, ai, t, dif);
     c64 v[8];
     digits(dif, shift, v);
+    PH(1);
     fwd_stage1(v, T1);
     exchange<1>(v, xb0, t, sync);
     fwd_stage2(v, T2);
     exchange<2>(v, xb1, t, sync);
     fwd_stage3(v);
+    PH(2);
     mbar_wait(&sm.full[g], i & 1);
+    PH(3);
     const c64* bk = sm.bkbuf[g];
 #pragma unroll
     for (int k2 = 0; k2 < 8; ++k2) {
@@ -534,12 +557,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
       sm.red[g][1][k2][t] = cmul(v[k2], bk[k2 * 128 + 64 + t]);
     }
     group_sync(bar_id);  // the group has read its key row
+    PH(4);
     if (t == 0 && i + 1 < kN) {
       mbar_expect_tx(&sm.full[g], kRowBytes);
       bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + row) * 1024, kRowBytes,
                &sm.full[g]);
     }
     __syncthreads();  // all three levels' partial products in red
+    PH(5);
     if (g >= 1) {     // the peer's polynomial: sum over levels, store remotely
       // (groups 1 and 2 take half the bins each: the peer's wait is shorter)
 #pragma unroll
@@ -560,18 +585,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
       for (int k2 = 0; k2 < 8; ++k2)
         v[k2] = cadd(cadd(sm.red[0][r][k2][t], sm.red[1][r][k2][t]), sm.red[2][r][k2][t]);
     }
+    PH(6);
     if (g == 0) mbar_wait(&sm.rbar[i & 1], (i >> 1) & 1);  // the peer's partial landed
+    PH(7);
     if (g == 0) {
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) v[k2] = cadd(v[k2], sm.recv[i & 1][k2][t]);
       inv_stageA(v);
       exchange<2>(v, sm.xbuf[1][0], t, sync);
+      PH(8);
       inv_stageB(v, T2);
       exchange<3>(v, sm.xbuf[2][0], t, sync);
+      PH(9);
       inv_stageC(v, T1);
+      PH(10);
       add_rounded(sm.acc, v, t);
+      PH(11);
     }
   }
+#ifdef CVM_PHASE_PROF
+  if (t == 0 && g < 2 && blockIdx.x < 148 * 2)
+    for (int k = 0; k < 12; ++k) g_pair_phase[blockIdx.x][g][k] = ph[k];
+#endif
   __syncthreads();
   // sample extraction: CTA 0 owns a (from ACC part 0), CTA 1 the b word
   uint32_t* out = xout + (size_t)job.out * kXlweStride;
@@ -584,6 +619,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
 }
 
 // ----------------------------------------------------------- launchers --
+#ifdef CVM_PHASE_PROF
+extern "C" __attribute__((visibility("default"))) int cvm_debug_pair_phases(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_pair_phase, sizeof(g_pair_phase));
+}
+#endif
+#undef PH
+
 cudaError_t launch_bk_to_fft(const uint32_t* bk, const c64* tw1, const c64* tw2, c64* bkf,
                              cudaStream_t s) {
   bk_to_fft_kernel<<<kN * kRows * 2, 64, 0, s>>>(bk, tw1, tw2, bkf);
