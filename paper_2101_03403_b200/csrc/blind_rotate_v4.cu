@@ -53,6 +53,22 @@ __device__ __forceinline__ TwBasesW load_wbases(const c64* tw4, int l) {
   return {ldg_c64(tw4 + 2 * l), ldg_c64(tw4 + 2 * l + 1)};
 }
 
+#ifdef CVM_PHASE_PROF
+// Developer instrumentation (tools/v4_phases.py): per-phase clock64 sums of
+// lane 0 of every warp, [cta][warp][phase].
+__device__ unsigned long long g_v4_phase[148][8][8];
+#define PH4(k)                                     \
+  do {                                             \
+    const long long now_ = clock64();              \
+    ph[k] += (unsigned long long)(now_ - last_);   \
+    last_ = now_;                                  \
+  } while (0)
+#else
+#define PH4(k) \
+  do {         \
+  } while (0)
+#endif
+
 // ----------------------------------------------------------------- K5 v4 --
 // One warp per key polynomial (i, row, o): forward warp FFT, the D factor of
 // the odd lanes removed (fft512w.cuh), scaled by 1/M.
@@ -147,6 +163,10 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
   prologue(job, slab, bar, acc0, acc1, l, 32, warp_sync, 0);
 
   int q = 0;
+#ifdef CVM_PHASE_PROF
+  unsigned long long ph[8] = {};
+  long long last_ = clock64();
+#endif
   for (int i = 0; i < kN; ++i) {
     __syncwarp();
     const int ai = bar[i];
@@ -192,6 +212,7 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
             v[a] = {u32_biased_to_double((pk[a] >> sh) & 127u, kDigitBias),
                     u32_biased_to_double((pk[a] >> (16 + sh)) & 127u, kDigitBias)};
         }
+        PH4(0);
         const int lo = opaque(l), eo = lo & 1;
         wfwd_stage1(v, opaque(tb));
 #pragma unroll
@@ -204,8 +225,10 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 + k] = shfl_xor1(v[8 + k]);
         wfwd_stage2b(v);
+        PH4(1);
         const int slot = q % S;
         mbar_wait(&sm.full[slot], (q / S) & 1);
+        PH4(2);
         const c64* bk = sm.ring[slot];
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -228,6 +251,7 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
             }
           }
         }
+        PH4(3);
       }
     }
 #pragma unroll 1
@@ -247,17 +271,30 @@ __global__ void __launch_bounds__(32 * kV4MaxWarps, 1) blind_rotate_kernel_v4(
       for (int k0 = 0; k0 < 16; ++k0) v[k0] = xb[wpos(k0, lo)];
       __syncwarp();
       winv_stage1(v, opaque(tb));
+      PH4(4);
       uint32_t* accp = o ? acc1 : acc0;
 #pragma unroll
       for (int a = 0; a < 16; ++a) {
         accp[l + 32 * a] += round_to_torus(v[a].x);
         accp[l + 32 * a + 512] += round_to_torus(v[a].y);
       }
+      PH4(5);
     }
   }
+#ifdef CVM_PHASE_PROF
+  if (l == 0 && blockIdx.x < 148)
+    for (int k = 0; k < 8; ++k) g_v4_phase[blockIdx.x][g][k] = ph[k];
+#endif
   __syncwarp();
   if (live) extract(acc0, acc1, xout + (size_t)job.out * kXlweStride, l, 32);
 }
+
+#ifdef CVM_PHASE_PROF
+extern "C" __attribute__((visibility("default"))) int cvm_debug_v4_phases(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_v4_phase, sizeof(g_v4_phase));
+}
+#endif
+#undef PH4
 
 // ----------------------------------------------------------- launchers --
 cudaError_t launch_bk_to_fft_v4(const uint32_t* bk, const c64* tw4, c64* bkf4, cudaStream_t s) {
