@@ -178,6 +178,10 @@ Bit GpuBackend::mux_gate_nl(Bit sel, Bit on_true, Bit on_false) {
 void GpuBackend::replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs,
                         Bit* handles) {
   std::lock_guard<std::mutex> lock(mu_);
+  if (!dag_region_.empty())  // region indices checked before anything is recorded
+    for (uint64_t i = 0; i < n; ++i)
+      if (nodes[i].region >= dag_region_.size())
+        throw InputError("dag region index out of range at dag node " + std::to_string(i + 1));
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const cvm_dag_node& d = nodes[i];
@@ -195,7 +199,6 @@ void GpuBackend::replay(const cvm_dag_node* nodes, uint64_t n, const Bit* inputs
     // otherwise)
     if (!dag_region_.empty() && d.region && is_gate(kind) && !d.input) {
       Node& nd = nodes_[h - 1];
-      if (d.region >= dag_region_.size()) throw InputError("dag region index out of range");
       region_recorded_[nd.region]--;
       nd.region = dag_region_[d.region];
       region_recorded_[nd.region]++;

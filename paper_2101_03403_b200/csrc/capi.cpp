@@ -560,6 +560,9 @@ int cvm_dag_batch_regions(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_node
     if (n_outputs) need(outputs, "outputs");
     for (uint64_t o = 0; o < n_outputs; ++o)
       if (outputs[o] == 0 || outputs[o] > n_nodes) throw InputError("output id out of range");
+    const uint64_t kMaxBits = UINT64_MAX / kLweWords;
+    if (batch && (n_in > kMaxBits / batch || n_outputs > kMaxBits / batch))
+      throw InputError("batch too large");
     if (in_words != batch * n_in * kLweWords)
       throw InputError("in_lwe holds " + std::to_string(in_words) + " words, the batch needs " +
                        std::to_string(batch * n_in * kLweWords));
@@ -592,6 +595,7 @@ int cvm_dag_batch_regions(cvm_ctx* c, const cvm_dag_node* nodes, uint64_t n_node
       bk.release_slots();  // the batch's slots are scratch: reuse them next call
     } catch (...) {
       context_sync(c->ctx);
+      bk.release_slots();  // the batch's scratch slots are not leaked on failure
       throw;
     }
     if (stats) *stats = bk.stats();

@@ -109,6 +109,22 @@ def test_fu_batch_reuses_its_scratch_slots(keyset, ctx):
     assert np.array_equal(sums, (np.arange(32) * 7 % 65536) + (np.arange(32) * 13 % 65536))
 
 
+def test_dag_batch_rejects_overflowing_batch(ctx):
+    """batch x inputs x 631 must not wrap around 2^64 into a small, matching
+    word count (capi.cpp cvm_dag_batch_regions)."""
+    import ctypes
+    from conftest import fu_dag
+    dag = fu_dag("add", 16)
+    batch = (1 << 64) // (dag.n_inputs * 631) + 1
+    wrapped = (batch * dag.n_inputs * 631) % (1 << 64)
+    outs = np.asarray(dag.outputs, np.uint64)
+    buf = np.zeros(max(wrapped, 1), np.uint32)
+    with pytest.raises(CvmInputError, match="batch too large"):
+        P._native.check(lib.cvm_dag_batch(ctx.handle, dag.nodes.ctypes.data, dag.n_nodes,
+                                          outs.ctypes.data, len(outs), ctypes.c_uint64(batch),
+                                          buf.ctypes.data, wrapped, buf.ctypes.data, 0, None))
+
+
 def test_concurrent_recording_threads(keyset, ctx):
     """gates.hpp:102-104: independent gates may be recorded concurrently."""
     bk = P.Backend(ctx, keyset)
@@ -218,3 +234,20 @@ def test_recorded_table_keeps_reference_regions(keyset, ctx):
     assert got == want
     assert bk.decrypt_word(out) == 16
     assert sum(v[1] for v in bk.regions().values()) == bk.stats()["executed"]
+
+
+def test_replay_rejects_bad_region_index_before_recording(keyset, ctx):
+    """A region index past the table's names is an InputError raised before any
+    gate of the table is recorded (backend.cpp GpuBackend::replay)."""
+    from conftest import fu_dag
+    dag = fu_dag("and", 4)
+    nodes = dag.nodes.copy()
+    gate = np.flatnonzero(nodes["input"] == 0)[0]
+    nodes["region"][gate] = 5
+    bad = P.Dag(nodes, dag.outputs, regions=["", "a", "b"])
+    bk = P.Backend(ctx, keyset)
+    ins = bk.import_lwe(keyset.encrypt_words([3, 5], 4, 9).reshape(-1, 631))
+    before = len(bk.nodes())
+    with pytest.raises(CvmInputError, match="region index out of range"):
+        bk.replay(bad, ins)
+    assert len(bk.nodes()) == before
