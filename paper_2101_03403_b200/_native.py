@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcvm_b200.so")
+# CVM_LIB_PATH: an alternative build of the same library (developer A/B runs)
+LIB_PATH = os.environ.get("CVM_LIB_PATH") or os.path.join(_HERE, "_lib", "libcvm_b200.so")
 
 LWE_N, POLY_N, LWE_WORDS = 630, 1024, 631
 BK_WORDS = 630 * 6 * 2 * 1024
