@@ -251,3 +251,23 @@ def test_replay_rejects_bad_region_index_before_recording(keyset, ctx):
     with pytest.raises(CvmInputError, match="region index out of range"):
         bk.replay(bad, ins)
     assert len(bk.nodes()) == before
+
+
+def test_empty_and_degenerate_inputs(keyset, ctx):
+    """Empty batches, levels, tables and handle lists are no-ops, and a table
+    whose outputs are its inputs (no gates) returns the input ciphertexts."""
+    from conftest import fu_dag
+    dag = fu_dag("add", 16)
+    out, st = P.dag_batch(ctx, dag, np.zeros((0, dag.n_inputs, 631), np.uint32))
+    assert out.shape == (0, len(dag.outputs), 631) and st["executed"] == 0
+    ctx.submit_level([])
+    ctx.sync()
+    bk = P.Backend(ctx, keyset)
+    assert bk.export_lwe([]).shape == (0, 631)
+    bk.evaluate([])
+    assert len(bk.replay(P.Dag(np.zeros(0, P.DAG_DTYPE), []), [])) == 0
+    # identity table: two input nodes, outputs = the inputs in swapped order
+    ident = P.Dag.from_rows([[0, 1, 0, 0, 0, 0, 0], [0, 1, 0, 0, 0, 0, 0]], [2, 1])
+    lwe = keyset.encrypt(np.array([1, 0]), 5)
+    got, st = P.dag_batch(ctx, ident, lwe.reshape(1, 2, 631))
+    assert np.array_equal(got[0], lwe[::-1]) and st["executed"] == 0
