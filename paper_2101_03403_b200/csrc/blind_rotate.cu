@@ -6,14 +6,17 @@
 //                               prologue, 630 CMux steps (gadget decomposition,
 //                               6 forward FFTs, 12 complex MACs against BK_i,
 //                               2 inverse FFTs, exact rounding), sample
-//                               extraction.  Organisations:
-//        v1   one bootstrap per 64-thread CTA, key read through L1 (baseline);
-//        v2   G bootstraps per CTA sharing a bulk-copy shared-memory key ring;
-//        v3   as v2, two transforms in flight per thread (throughput default,
-//             with generated twiddles and held differences: variant 5144);
-//        wide one bootstrap on 384 threads, the six gadget rows transformed
-//             concurrently (latency, 75-148 bootstraps);
-//        pair one bootstrap on a 2-SM cluster (latency, <= 74 bootstraps).
+//                               extraction.  Organisations in this file (the
+//                               64-thread FFT of fft512.cuh):
+//        v3   (5247) 4 bootstraps per CTA sharing a bulk-copy shared-memory key
+//             ring, two transforms in flight per thread, generated twiddles
+//             (the remainder of a wide level after its full v4 waves);
+//        wide (9) one bootstrap on 384 threads, the six gadget rows transformed
+//             concurrently (latency, 75-296 bootstraps);
+//        pair (96) one bootstrap on a 2-SM cluster (latency, <= 74 bootstraps).
+//   The throughput kernel (v4, one bootstrap per warp) is blind_rotate_v4.cu.
+//   Retired round-1 organisations (v1: key through L1; v2: the ring without
+//   paired transforms) are measured in profiles/r01_variant_sweep.txt.
 //
 // All variants produce bit-identical ciphertexts (tests/test_gpu_parity.py).
 // DESIGN.md section 4 gives the roofline of each kernel; measured variant
@@ -155,10 +158,10 @@ __device__ __forceinline__ TwBases tw_bases(const c64* tw1, int t) {
 }
 
 // ---------------------------------------------------------- K1 + K2, v3 --
-// As v2, but every thread runs two transforms at once: the forward FFTs of
-// the same gadget level of both TRLWE parts (rows p and 3+p), and the two
-// inverse FFTs -- twice the independent FP64 work between barriers, the same
-// number of barriers.  Exchange buffers are single-buffered (a WAR barrier
+// G bootstraps per CTA share a bulk-copy key ring, and every thread runs two
+// transforms at once: the forward FFTs of the same gadget level of both TRLWE
+// parts (rows p and 3+p), and the two inverse FFTs -- twice the independent
+// FP64 work between barriers, the same number of barriers.  Exchange buffers are single-buffered (a WAR barrier
 // follows each exchange).  The key ring is consumed in pair order (rows 0,3,
 // 1,4, 2,5 of each step) and the producer keeps one pair in flight.
 template <int G, int S>
