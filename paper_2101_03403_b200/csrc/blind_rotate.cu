@@ -559,14 +559,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
       sm.red[g][0][k2][t] = cmul(v[k2], bk[k2 * 128 + t]);
       sm.red[g][1][k2][t] = cmul(v[k2], bk[k2 * 128 + 64 + t]);
     }
-    group_sync(bar_id);  // the group has read its key row
+    __syncthreads();  // all three levels' partial products in red (and keys read)
     PH(4);
-    if (t == 0 && i + 1 < kN) {
+    if (t == 0 && i + 1 < kN) {  // next row's copy lands outside every group's MAC
       mbar_expect_tx(&sm.full[g], kRowBytes);
       bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + row) * 1024, kRowBytes,
                &sm.full[g]);
     }
-    __syncthreads();  // all three levels' partial products in red
     PH(5);
     if (g >= 1) {     // the peer's polynomial: sum over levels, store remotely
       // (groups 1 and 2 take half the bins each: the peer's wait is shorter)

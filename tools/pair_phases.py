@@ -14,9 +14,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2101_03403_b200 as P  # noqa: E402
 from paper_2101_03403_b200._native import check, lib  # noqa: E402
 
-NAMES = ["top barrier", "rotate+digits", "fwd FFT", "key wait", "MAC+group sync",
-         "all-partials barrier", "own sum / send", "peer wait", "inv A+ex",
-         "inv B+ex", "inv C", "add_rounded"]
+NAMES = ["top barrier", "rotate+digits", "fwd FFT", "key wait",
+         "MAC + all-partials barrier", "next-row copy issue", "own sum / send", "peer wait",
+         "inv A+ex", "inv B+ex", "inv C", "add_rounded"]
 
 
 def main():
