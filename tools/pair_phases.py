@@ -31,7 +31,7 @@ def main():
     ctx.upload(base + n, ks.encrypt(b, 2))
     gates = [("NAND", [(base + i, 1, 0), (base + n + i, 1, 0)], base + 2 * n + i)
              for i in range(n)]
-    check(lib.cvm_set_br_variant(96))
+    check(lib.cvm_set_br_variant(int(os.environ.get("VARIANT", 96))))
     ctx.set_profiling(True)
     for _ in range(3):
         ctx.reset_stats()
