@@ -1,6 +1,6 @@
 """Static SASS instruction counts per kernel of the built library
 (cuobjdump -sass), restricted to the mnemonics that show which sm_100a
-features each kernel uses.  Writes profiles/r01_sass_evidence.txt.
+features each kernel uses.  Writes OUT (default profiles/r02_sass_evidence.txt).
 
     python tools/sass_evidence.py [OUT]
 """
@@ -23,7 +23,7 @@ SHFL = warp shuffle (the v4 warp FFT's lane-pair exchange); BAR = CTA / named ba
 
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles",
-                                                              "r01_sass_evidence.txt")
+                                                              "r02_sass_evidence.txt")
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True,
                           check=True).stdout
     names = dict(re.findall(r"Function : (\S+)", sass) and [])
