@@ -567,11 +567,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
                &sm.full[g]);
     }
     PH(5);
-    if (g >= 1) {     // the peer's polynomial: sum over levels, store remotely
-      // (groups 1 and 2 take half the bins each: the peer's wait is shorter)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k2 = 4 * (g - 1) + kk;
+    {  // the peer's polynomial: sum over levels, store remotely -- every group
+       // takes a share of the bins (group 0 the smallest: it owns the inverse)
+      auto send = [&](int k2) {
         const c64 x = cadd(cadd(sm.red[0][r ^ 1][k2][t], sm.red[1][r ^ 1][k2][t]),
                            sm.red[2][r ^ 1][k2][t]);
         const uint32_t a = peer_recv_a + uint32_t(((i & 1) * 512 + k2 * 64 + t) * 16);
@@ -581,8 +579,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 * kL, 1)
             "l"(__double_as_longlong(x.x)), "l"(__double_as_longlong(x.y)),
             "r"(peer_rbar_a + uint32_t(8 * (i & 1)))
             : "memory");
-      }
-    } else if (g == 0) {  // my polynomial: local part of the sum
+      };
+      // bins k2 sent by groups 0 / 1 / 2: 2 / 3 / 3 (0 / 4 / 4: 1.428 ms per
+      // 74-gate level, 1 / 4 / 3: 1.423, 2 / 3 / 3: 1.410, 3 / 3 / 2: 1.413)
+      constexpr int n0 = 2, n1 = 3;
+      const int first = g == 0 ? 0 : g == 1 ? n0 : n0 + n1;
+      const int count = g == 0 ? n0 : g == 1 ? n1 : 8 - n0 - n1;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        if (kk < count) send(first + kk);
+    }
+    if (g == 0) {  // my polynomial: local part of the sum
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2)
         v[k2] = cadd(cadd(sm.red[0][r][k2][t], sm.red[1][r][k2][t]), sm.red[2][r][k2][t]);
