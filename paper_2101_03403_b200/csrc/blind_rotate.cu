@@ -700,10 +700,10 @@ cudaError_t launch_blind_rotate(int variant, const BrJob* jobs, int count, const
     // per SM gives each its own CTA; wide levels use the v4 throughput
     // kernel (blind_rotate_v4.cu) with the remainder split off below.
     constexpr int kSms = kBrSms;
-    if (count <= kSms / 2) {
-      variant = 96;  // one bootstrap per 2-SM cluster: 1.53 vs 2.27 ms
-    } else if (count <= 2 * kSms) {
-      variant = 9;  // one or two rounds of one bootstrap per SM (4.55 ms for 296; v2: 4.82)
+    if (count <= 2 * kSms) {
+      // pair rounds of 74 (1.41 ms) or wide rounds of 148 (2.27 ms): pair up
+      // to 74 and for 149-222 (4.18 vs 4.54 ms), wide otherwise
+      variant = br_latency_pair(count) ? 96 : 9;
     } else {
       // Wide levels: the v4 kernel (one bootstrap per warp, 8 per SM) works
       // in waves of 8 x 148 bootstraps (~11.4 ms; with 5-7 warps per SM a
@@ -735,8 +735,11 @@ cudaError_t launch_blind_rotate(int variant, const BrJob* jobs, int count, const
         if (e != cudaSuccess) return e;
         done += n;
       }
-      if (b1 && done < count) return launch_wide(jobs + done, count - done, slab, bkf, tw1, tw2,
-                                                  xout, s);
+      if (b1 && done < count) {
+        const int n = count - done;
+        return br_latency_pair(n) ? launch_pair(jobs + done, n, slab, bkf, tw1, tw2, xout, s)
+                                  : launch_wide(jobs + done, n, slab, bkf, tw1, tw2, xout, s);
+      }
       return cudaSuccess;
     }
   }

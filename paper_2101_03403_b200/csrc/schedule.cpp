@@ -5,24 +5,31 @@
 
 namespace cvm {
 
+int br_latency_cost(int n) {
+  if (n <= 0) return 0;
+  const int pair = (n + kBrPair - 1) / kBrPair * kBrTP, wide = (n + kBrSms - 1) / kBrSms * kBrT1;
+  return std::min(pair, wide);
+}
+bool br_latency_pair(int n) {
+  return (n + kBrPair - 1) / kBrPair * kBrTP < (n + kBrSms - 1) / kBrSms * kBrT1;
+}
+
 int br_remainder_plan(int rest, int* n8, int* n4, int* n1) {
   int best = rest > 0 ? 1 << 30 : 0, b8 = 0, b4 = 0, b1 = 0;
   for (int a = 0; a <= 1 && rest > 0; ++a)
-    for (int b = 0; b <= 2; ++b)
-      for (int c = 0; c <= 4; ++c) {
-        if (a * kBrWave8 + b * kBrWave4 + c * kBrSms < rest) continue;
-        const int cost = a * kBrT8 + b * kBrT4 + c * kBrT1;
-        if (cost < best) best = cost, b8 = a, b4 = b, b1 = c;
-      }
+    for (int b = 0; b <= 2; ++b) {
+      const int left = std::max(0, rest - a * kBrWave8 - b * kBrWave4);
+      if (left > 4 * kBrSms) continue;
+      const int cost = a * kBrT8 + b * kBrT4 + br_latency_cost(left);
+      if (cost < best) best = cost, b8 = a, b4 = b, b1 = left;
+    }
   if (n8) *n8 = b8, *n4 = b4, *n1 = b1;
   return best;
 }
 
 int br_level_cost(int boots) {
   if (boots <= 0) return 0;
-  if (boots <= kBrSms / 2) return 15;  // pair kernel, 1.53 ms
-  if (boots <= kBrSms) return kBrT1;       // one bootstrap per SM
-  if (boots <= 2 * kBrSms) return 2 * kBrT1;  // two rounds of it
+  if (boots <= 2 * kBrSms) return br_latency_cost(boots);
   const int full = boots / kBrWave8;
   return full * kBrT8 + br_remainder_plan(boots - full * kBrWave8, nullptr, nullptr, nullptr);
 }

@@ -10,15 +10,23 @@
 
 namespace cvm {
 
-// A v4 wave of 8 x 148 bootstraps, a v3 round of 4 x 148 and a latency round
-// of 148 (one bootstrap per SM), in 0.1 ms.
+// A v4 wave of 8 x 148 bootstraps, a v3 round of 4 x 148, a wide-kernel round
+// of 148 (one bootstrap per SM) and a pair-kernel round of 74 (one bootstrap
+// per 2-SM cluster), in 0.1 ms.
 constexpr int kBrSms = 148, kBrWave8 = 8 * kBrSms, kBrWave4 = 4 * kBrSms;
-constexpr int kBrT8 = 113, kBrT4 = 58, kBrT1 = 23;
+constexpr int kBrPair = kBrSms / 2;
+constexpr int kBrT8 = 113, kBrT4 = 58, kBrT1 = 23, kBrTP = 14;
+
+// Latency kernels for n bootstraps: rounds of the pair kernel or of the wide
+// kernel, whichever finishes first (pair for n <= 74 and 149-222: measured
+// 1.41 / 4.18 ms vs wide 2.27 / 4.54 ms).
+int br_latency_cost(int n);
+bool br_latency_pair(int n);
 
 // The remainder of a wide level after its full v4 waves: at most one more v4
-// wave, two v3 rounds and four latency rounds, the cheapest combination that
-// covers `rest`.  Returns its cost (0.1 ms); the counts go to n8/n4/n1 if
-// non-null.
+// wave, two v3 rounds and up to 592 bootstraps on the latency kernels, the
+// cheapest combination that covers `rest`.  Returns its cost (0.1 ms); the v4
+// waves / v3 rounds / latency bootstraps go to n8/n4/n1 if non-null.
 int br_remainder_plan(int rest, int* n8, int* n4, int* n1);
 
 // Device time (0.1 ms) of one level of `boots` bootstraps under the
