@@ -12,8 +12,9 @@
 //             ring, two transforms in flight per thread, generated twiddles
 //             (the remainder of a wide level after its full v4 waves);
 //        wide (9) one bootstrap on 384 threads, the six gadget rows transformed
-//             concurrently (latency, 75-296 bootstraps);
-//        pair (96) one bootstrap on a 2-SM cluster (latency, <= 74 bootstraps).
+//             concurrently (latency, 75-148 and 223-296 bootstraps);
+//        pair (96) one bootstrap on a 2-SM cluster (latency, <= 74 and 149-222
+//             bootstraps: rounds of 74; schedule.hpp br_latency_pair).
 //   The throughput kernel (v4, one bootstrap per warp) is blind_rotate_v4.cu.
 //   Retired round-1 organisations (v1: key through L1; v2: the ring without
 //   paired transforms) are measured in profiles/r01_variant_sweep.txt.
