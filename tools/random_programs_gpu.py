@@ -21,18 +21,21 @@ sys.path.insert(0, os.path.join(REPO, "integration"))
 import paper_2101_03403_b200 as P  # noqa: E402
 import refshim  # noqa: E402
 
-PLAN = [(8, 200, 64), (16, 100, 32)]  # (word size, programs, memory images per program)
+PLAN = [(8, 200, 64), (16, 100, 32), (32, 20, 8)]  # (word size, programs, images)
 N_MEM, N_REGS = 4, 8
 
 
 def main():
     out_path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/random_programs.json"
+    only = {int(x) for x in sys.argv[2:]}  # optional word sizes to run
     ks = P.KeySet(9)
     ctx = P.Context(0)
     ctx.upload_keyset(ks)
     rng = np.random.default_rng(2026)
     res = {}
     for w, n_prog, n_img in PLAN:
+        if only and w not in only:
+            continue
         bad_runs, runs, gates, t0 = 0, 0, 0, time.time()
         for k in range(n_prog):
             prog = refshim.random_program(rng, w, n_mem=N_MEM, n_regs=N_REGS)
