@@ -396,11 +396,6 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
       pa[k2] = cmul(v[k2], bk[k2 * 128 + t]);
       pb[k2] = cmul(v[k2], bk[k2 * 128 + 64 + t]);
     }
-    group_sync(bar_id);  // the whole group has read its key row
-    if (t == 0 && i + 1 < kN) {
-      mbar_expect_tx(&sm.full[g], kRowBytes);
-      bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + g) * 1024, kRowBytes, &sm.full[g]);
-    }
     // two-phase reduction of the six partials into three pair sums
     if (part == 1) {
 #pragma unroll
@@ -409,7 +404,11 @@ __global__ void __launch_bounds__(64 * kRows, 1) blind_rotate_wide_kernel(
         sm.red[p][1][k2][t] = pb[k2];
       }
     }
-    __syncthreads();
+    __syncthreads();  // (every group has read its key row)
+    if (t == 0 && i + 1 < kN) {  // the next row lands outside every group's MAC
+      mbar_expect_tx(&sm.full[g], kRowBytes);
+      bulk_g2s(sm.bkbuf[g], bkf + ((size_t)(i + 1) * kRows + g) * 1024, kRowBytes, &sm.full[g]);
+    }
     if (part == 0) {
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) {
