@@ -74,11 +74,12 @@ def test_kernel_variants_bit_identical(variant, keyset, ctx, oracle_keys):
     assert np.array_equal(keyset.decrypt(out), a ^ (1 - b))
 
 
-@pytest.mark.parametrize("n", [700, 1224, 1584, 1984])
+@pytest.mark.parametrize("n", [192, 700, 1224, 1376, 1584, 1984])
 def test_wide_level_planner_bit_identical(n, keyset, ctx, oracle_keys):
     """Auto selection of a wide level: full waves of the v4 warp kernel, then
     the remainder on another v4 wave with fewer warps per SM, on v3 rounds
-    and/or latency rounds (blind_rotate.cu).  The sizes hit each combination;
+    and/or latency rounds -- pair or wide (blind_rotate.cu; 192 alone and as
+    the remainder of 1376 take three pair rounds).  The sizes hit each combination;
     the result must equal the whole level on one kernel (6085, pinned to the
     oracle by test_kernel_variants_bit_identical)."""
     from paper_2101_03403_b200._native import lib, check
